@@ -1,0 +1,329 @@
+"""DecDEC oracle (float64 NumPy) -- TEST INFRASTRUCTURE ONLY, see oracle/__init__.py.
+
+Plain statement of the decode-step hot path of DecDEC (arXiv 2412.20185).
+Citations: ``P:n`` = /root/reference/PAPER.md line n, ``S:n`` = SPEC.md line n;
+``L#`` = the readings ledger in DESIGN.md (copied from SURVEY.md §8(c)).
+
+    o = W_hat x + sum_{i in S(x)} x_i * R_hat[i, :]
+
+Functions and their pins (tests/test_oracle_*.py):
+
+  O1 quantize_base      pinned: zero fixed point, exactly-representable groups give
+                        R = 0, idempotence on full-range groups, hand-worked group
+                        (tests/golden/base_quant_group.txt), RTN bound |R| <= s/2.
+  O2 residual           pinned through O5 k=d_in invariant (W x recovered).
+  O3 quantize_residual  pinned: S:63 worked example, brute-force grid argmin with an
+                        independent scalar loop, clip bound, zero column, r16 round trip.
+  O4 topk_ref           pinned: S:129-130 examples, brute force over every k-subset for
+                        d_in <= 12, threshold/dominance property at large d_in,
+                        P:255 chunk example (4096, k_chunk 32 -> 128).
+  O5 decdec_linear_ref  pinned: R=0 weights give y = W x for every k (numpy matmul of
+                        the original W), k = d_in with r_bits = 16 recovers W x within
+                        L9, single channel x_i = 2 gives 2 x row i, linearity
+                        over disjoint selections, empty selection.
+  O6 pack_*_ref         pinned: hand-derived golden words (tests/golden/pack_words.txt)
+                        and unpack(pack(q)) == q round trips.
+
+Parity unpinned: none of the functions above; large-shape GEMV values have no
+paper-printed worked example (P:147-152 is figure-only), so they rest on the
+definitions plus the invariants listed.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+GROUP = 128  # L5: AWQ-style group of 128 input channels per output channel
+
+
+# ----------------------------------------------------------------------------- scalars
+def fp16_rne(v):
+    """Round float64 values to the nearest binary16 (ties to even), returned as float64.
+
+    NumPy's float64 -> float16 cast is IEEE round-to-nearest-even (pinned in tests).
+    """
+    return np.asarray(v, dtype=np.float64).astype(np.float16).astype(np.float64)
+
+
+def round_half_away(v):
+    """round_to_int of the residual quantizer: half away from zero (ledger L4)."""
+    v = np.asarray(v, dtype=np.float64)
+    a = np.abs(v)
+    f = np.floor(a)
+    r = f + ((a - f) >= 0.5)
+    return np.sign(v) * r
+
+
+# ----------------------------------------------------------------------------- O1/O2
+def quantize_base(W16, bits: int, group: int = GROUP):
+    """O1: RTN group-wise asymmetric base quantizer (stand-in for AWQ; L5).
+
+    W16: float16 [d_in, d_out] (rows = input channels).  For every group g of
+    ``group`` consecutive input channels and every output column j (all in float64):
+        v   = W[g*G:(g+1)*G, j]
+        rng = max(max v - min v, 1e-5)
+        s   = fp16_rne(rng / (2^b - 1))
+        z   = clip(rne(-min v / s), 0, 2^b - 1)
+        q   = clip(rne(v / s) + z, 0, 2^b - 1)
+    Returns (q uint8 [d_in, d_out], s float16 [G, d_out], z uint8 [G, d_out]).
+    """
+    W = np.asarray(W16, dtype=np.float16).astype(np.float64)
+    d_in, d_out = W.shape
+    if d_in % group:
+        raise ValueError("group must divide d_in")
+    qmax = (1 << bits) - 1
+    G = d_in // group
+    Wg = W.reshape(G, group, d_out)
+    vmax = Wg.max(axis=1)
+    vmin = Wg.min(axis=1)
+    rng = np.maximum(vmax - vmin, 1e-5)
+    s = fp16_rne(rng / qmax)
+    z = np.clip(np.rint(-vmin / s), 0, qmax)
+    q = np.clip(np.rint(Wg / s[:, None, :]) + z[:, None, :], 0, qmax)
+    return (q.reshape(d_in, d_out).astype(np.uint8), s.astype(np.float16), z.astype(np.uint8))
+
+
+def dequantize_base(q, s, z, group: int = GROUP):
+    """W_hat = s * (q - z), exact in float64 (P:134 'quantized weights')."""
+    q = np.asarray(q, dtype=np.float64)
+    d_in, d_out = q.shape
+    G = d_in // group
+    s64 = np.asarray(s, dtype=np.float16).astype(np.float64)
+    z64 = np.asarray(z, dtype=np.float64)
+    return (s64[:, None, :] * (q.reshape(G, group, d_out) - z64[:, None, :])).reshape(d_in, d_out)
+
+
+def residual(W16, W_hat):
+    """O2: R = W - W_hat in float64 (exact)."""
+    return np.asarray(W16, dtype=np.float16).astype(np.float64) - np.asarray(W_hat, dtype=np.float64)
+
+
+# ----------------------------------------------------------------------------- O3
+def quantize_residual(R, r_bits: int = 4):
+    """O3: residual quantizer Q_r (ledger L1, L4).
+
+    r_bits = 4: per output column j (P:222 'for each output channel (i.e., column)'),
+        m = max |R[:, j]|;  m == 0 -> S_j = 1, codes 0
+        for t = 0..127:  g = 0.30 + 0.70 t / 127
+                         S_t = fp16_rne(m g / 7)   (skip if 0)   (L4: rounded before use)
+                         c   = clip(round_half_away(R / S_t), -7, 7)
+                         e_t = sum (R - S_t c)^2
+        S_j = S_argmin (ties -> larger t).
+      Returns (codes int8 [d_in, d_out], S float16 [d_out]).
+    r_bits = 16: returns fp16_rne(R) as float16 [d_in, d_out] (Table 3 FP16 column).
+    """
+    R = np.asarray(R, dtype=np.float64)
+    if r_bits == 16:
+        return R.astype(np.float16)
+    if r_bits != 4:
+        raise ValueError("r_bits must be 4 or 16")
+    d_in, d_out = R.shape
+    m = np.abs(R).max(axis=0)
+    best_e = np.full(d_out, np.inf)
+    best_S = np.ones(d_out)
+    best_c = np.zeros((d_in, d_out))
+    for t in range(128):
+        g = 0.30 + 0.70 * t / 127.0
+        S_t = fp16_rne(m * g / 7.0)
+        ok = S_t > 0
+        Sd = np.where(ok, S_t, 1.0)
+        c = np.clip(round_half_away(R / Sd), -7, 7)
+        e = ((R - Sd * c) ** 2).sum(axis=0)
+        take = ok & (e <= best_e)  # '<=' while t ascends: ties go to the larger t
+        best_e = np.where(take, e, best_e)
+        best_S = np.where(take, S_t, best_S)
+        best_c[:, take] = c[:, take]
+    zero = m == 0
+    best_S[zero] = 1.0
+    best_c[:, zero] = 0
+    return best_c.astype(np.int8), best_S.astype(np.float16)
+
+
+def dequantize_residual_rows(codes, S, rows):
+    """R_hat[rows, :] = S_j * codes[rows, j]; order follows ``rows``."""
+    rows = np.asarray(rows, dtype=np.int64)
+    S64 = np.asarray(S, dtype=np.float16).astype(np.float64)
+    return np.asarray(codes, dtype=np.float64)[rows, :] * S64[None, :]
+
+
+# ----------------------------------------------------------------------------- O4
+def k_from_kchunk(k_chunk: int, d_in: int) -> int:
+    """k = floor(k_chunk * d_in / 1024) (10% of 14336 -> 1433; ledger L3)."""
+    return (int(k_chunk) * int(d_in)) // 1024
+
+
+def _keys(x16):
+    return (np.asarray(x16, dtype=np.float16).view(np.uint16) & np.uint16(0x7FFF)).astype(np.int64)
+
+
+def topk_ref(x16, k: int, chunk: int = 0):
+    """O4: exact Top-K of |x| ("Exact"; step 1 of P:207; ledger L2).
+
+    Magnitude = 15-bit fp16 key bits(x) & 0x7FFF (+0 and -0 tie).  Order by
+    (key desc, index asc); take the first k.  chunk = 0: global selection of k.
+    chunk = C > 0: the same rule inside every contiguous C-channel chunk with quota
+    min(k, chunk length) -- here ``k`` is k_chunk (short last chunk).
+    Returns (idx int32 ascending, xs float16 = x[idx]).
+    """
+    x16 = np.asarray(x16, dtype=np.float16)
+    key = _keys(x16)
+    n = key.shape[0]
+    if k < 0:
+        raise ValueError("k < 0")
+    segs = [(0, n)] if chunk == 0 else [(a, min(a + chunk, n)) for a in range(0, n, chunk)]
+    if chunk == 0 and k > n:
+        raise ValueError("k > d_in")
+    if chunk and k > chunk:
+        raise ValueError("k_chunk > chunk")
+    out = []
+    for a, b in segs:
+        q = min(k, b - a)
+        order = np.argsort(-key[a:b], kind="stable")  # stable: equal keys keep index order
+        out.append(np.sort(order[:q]) + a)
+    idx = np.concatenate(out).astype(np.int32) if out else np.zeros(0, np.int32)
+    return idx, x16[idx]
+
+
+# ----------------------------------------------------------------------------- O5
+def decdec_linear_ref(q, s, z, x16, k: int, chunk: int = 0, rc=None, rS=None, r16=None):
+    """O5: y = W_hat x + sum_{i in S} x_i R_hat[i, :] in float64 (P:204-207 steps 1-4).
+
+    q uint8 [d_in, d_out], s fp16 [G, d_out], z uint8 [G, d_out]: base weights (O1 format).
+    Residual either 4-bit (rc int8 [d_in, d_out], rS fp16 [d_out]) or fp16 (r16 [d_in, d_out]).
+    Any column subset may be passed (columns are independent), which is how full-size
+    parity samples outputs.
+    Returns dict: idx, xs (selection), ob, odec, y64, y16 (fp16_rne of y64), A
+    (A_j = sum_i |W_hat_ij x_i| + sum_{i in S} |R_hat_ij x_i|, the L9 scale).
+    """
+    W_hat = dequantize_base(q, s, z)
+    x = np.asarray(x16, dtype=np.float16).astype(np.float64)
+    ob = x @ W_hat                                   # step: o_b = W_hat x
+    A = np.abs(x) @ np.abs(W_hat)
+    idx, xs = topk_ref(x16, k, chunk)                # step 1: sc_indices
+    if r16 is not None:
+        Rrows = np.asarray(r16, dtype=np.float16).astype(np.float64)[idx.astype(np.int64), :]
+    elif rc is not None:
+        Rrows = dequantize_residual_rows(rc, rS, idx)  # step 2: fetch R_hat[S, :]
+    else:
+        Rrows = np.zeros((len(idx), W_hat.shape[1]))
+    xs64 = xs.astype(np.float64)
+    odec = xs64 @ Rrows                              # step 3: o_dec
+    A = A + np.abs(xs64) @ np.abs(Rrows)
+    y64 = ob + odec                                  # step 4: o = o_b + o_dec
+    return dict(idx=idx, xs=xs, ob=ob, odec=odec, y64=y64, y16=y64.astype(np.float16), A=A)
+
+
+def decdec_linear_ref_cols(q, s, z, x16, k, cols, chunk=0, rc=None, rS=None, r16=None):
+    """O5 on a subset of output columns (sampled full-size parity)."""
+    cols = np.asarray(cols, dtype=np.int64)
+    return decdec_linear_ref(
+        q[:, cols], s[:, cols], z[:, cols], x16, k, chunk,
+        rc=None if rc is None else rc[:, cols],
+        rS=None if rS is None else np.asarray(rS)[cols],
+        r16=None if r16 is None else r16[:, cols],
+    )
+
+
+def tolerance_ok(y16, y64, A):
+    """Ledger L9: |y16 - y*| <= 1e-3 * max(|y*|, 2^-12 A_j, 2^-14) (BJ 'max relative error 1e-3')."""
+    y = np.asarray(y16, dtype=np.float16).astype(np.float64)
+    y64 = np.asarray(y64, dtype=np.float64)
+    bound = 1e-3 * np.maximum(np.maximum(np.abs(y64), 2.0 ** -12 * np.asarray(A)), 2.0 ** -14)
+    err = np.abs(y - y64)
+    return err <= bound, err, bound
+
+
+# ----------------------------------------------------------------------------- O6 packing
+# Layouts (DESIGN.md ledger L6).  Implemented here bit by bit, independently of the C++ packers.
+def _w4_bitpos(c):
+    """channel c (0..7) of an 8-channel word sits at bit 4*(c>>1) + 16*(c&1)."""
+    return 4 * (c >> 1) + 16 * (c & 1)
+
+
+def pack_w4k_ref(q):
+    """W4K: q uint8 [d_in, d_out] codes in [0,15] -> uint32 [d_out, d_in/8] (K-major rows)."""
+    q = np.asarray(q, dtype=np.uint64)
+    d_in, d_out = q.shape
+    qt = q.T.reshape(d_out, d_in // 8, 8)
+    out = np.zeros((d_out, d_in // 8), dtype=np.uint64)
+    for c in range(8):
+        out |= (qt[:, :, c] & 0xF) << np.uint64(_w4_bitpos(c))
+    return out.astype(np.uint32)
+
+
+def unpack_w4k_ref(words, d_in):
+    words = np.asarray(words, dtype=np.uint64)
+    d_out = words.shape[0]
+    q = np.zeros((d_out, d_in // 8, 8), dtype=np.uint8)
+    for c in range(8):
+        q[:, :, c] = (words >> np.uint64(_w4_bitpos(c))) & 0xF
+    return q.reshape(d_out, d_in).T.copy()
+
+
+def _w3_fields():
+    """List of (channel, word t, [bit positions of code bits 0,1,2])."""
+    fields = []
+    for c in range(32):
+        if c < 30:
+            t, r = divmod(c, 10)
+            p, h = divmod(r, 2)
+            base = 16 * h + 3 * p
+            fields.append((c, [(t, base), (t, base + 1), (t, base + 2)]))
+        else:
+            h = c - 30
+            fields.append((c, [(0, 16 * h + 15), (1, 16 * h + 15), (2, 16 * h + 15)]))
+    return fields
+
+
+def pack_w3k_ref(q):
+    """W3K: q uint8 [d_in, d_out] codes in [0,7] -> uint32 [d_out, 3*d_in/32].
+
+    Per 32-channel slice, 3 words.  Channel c < 30: word c//10, half h = (c%10)%2,
+    position p = (c%10)//2, bits 16h+3p .. 16h+3p+2.  Channels 30, 31 (h = c-30):
+    code bit b lives at word b, bit 16h + 15.
+    """
+    q = np.asarray(q, dtype=np.uint64)
+    d_in, d_out = q.shape
+    qt = q.T.reshape(d_out, d_in // 32, 32)
+    out = np.zeros((d_out, d_in // 32, 3), dtype=np.uint64)
+    for c, bits in _w3_fields():
+        for b, (t, pos) in enumerate(bits):
+            out[:, :, t] |= ((qt[:, :, c] >> np.uint64(b)) & 1) << np.uint64(pos)
+    return out.reshape(d_out, 3 * d_in // 32).astype(np.uint32)
+
+
+def unpack_w3k_ref(words, d_in):
+    words = np.asarray(words, dtype=np.uint64)
+    d_out = words.shape[0]
+    w = words.reshape(d_out, d_in // 32, 3)
+    q = np.zeros((d_out, d_in // 32, 32), dtype=np.uint64)
+    for c, bits in _w3_fields():
+        for b, (t, pos) in enumerate(bits):
+            q[:, :, c] |= ((w[:, :, t] >> np.uint64(pos)) & 1) << np.uint64(b)
+    return q.reshape(d_out, d_in).T.astype(np.uint8).copy()
+
+
+def pack_rq_ref(codes):
+    """Rq: residual codes int8 [d_in, d_out] in [-7,7] -> uint32 [d_in, d_out/8].
+
+    Row = input channel, contiguous.  Nibble = c + 8 (offset binary); column c
+    of an 8-column word at bit 4*(c>>1) + 16*(c&1) (same interleave as W4K).
+    """
+    c = np.asarray(codes, dtype=np.int64)
+    if np.any(np.abs(c) > 7):
+        raise ValueError("residual codes outside [-7, 7]")
+    d_in, d_out = c.shape
+    u = (c + 8).astype(np.uint64).reshape(d_in, d_out // 8, 8)
+    out = np.zeros((d_in, d_out // 8), dtype=np.uint64)
+    for cc in range(8):
+        out |= u[:, :, cc] << np.uint64(_w4_bitpos(cc))
+    return out.astype(np.uint32)
+
+
+def unpack_rq_ref(words, d_out):
+    words = np.asarray(words, dtype=np.uint64)
+    d_in = words.shape[0]
+    c = np.zeros((d_in, d_out // 8, 8), dtype=np.int64)
+    for cc in range(8):
+        c[:, :, cc] = ((words >> np.uint64(_w4_bitpos(cc))) & 0xF).astype(np.int64) - 8
+    return c.reshape(d_in, d_out).astype(np.int8)

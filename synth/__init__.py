@@ -1,0 +1,15 @@
+"""Seeded synthetic inputs shared by the oracle tests and the CUDA path.
+
+Holds NO arithmetic of the DecDEC method: only random draws with the shapes and
+distributions of the paper's workloads.
+"""
+
+from .inputs import (  # noqa: F401
+    SHAPES,
+    layer_seed,
+    gen_weight_fp16,
+    gen_activations,
+    gen_special_activations,
+    gen_perf_layer,
+    model_layers,
+)

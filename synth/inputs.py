@@ -1,0 +1,103 @@
+"""Seeded synthetic generators (no method arithmetic).  Recipe: DESIGN.md "Input recipe".
+
+Weights   W_ij ~ N(0, 0.02^2) x per-column LogNormal(0, 0.25), cast to fp16.
+Acts      x_i = sigma_i * t_i, sigma_i ~ LogNormal(0, 0.5) fixed per layer, t_i ~ Student-t(3)
+          per step, plus 8 persistent massive-outlier channels per layer with sigma x 20
+          (qkv/o/gu inputs) or x 200 (down input); clamp to +-2^15; fp16.  (S:523 style,
+          'outlier-heavy activations shaped like Llama-3 decode', BASELINE.json.)
+Perf      stored quantities drawn directly: q ~ U[0, 2^b-1];
+layers    z ~ U{3,4} (3-bit) / U{7,8} (4-bit); s = fp16(0.02*sqrt(12)/2^b * LogNormal(0,0.25))
+          per group; residual codes ~ U[-7,7]; S_j = fp16(median_g s_gj / 14).
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+# Layer shapes d_in x d_out (W is logically [d_in, d_out], rows = input channels).
+SHAPES = {
+    "config1": {"l": (1024, 1024)},
+    "llama3_8b": {
+        "q": (4096, 4096), "k": (4096, 1024), "v": (4096, 1024), "o": (4096, 4096),
+        "gate": (4096, 14336), "up": (4096, 14336), "down": (14336, 4096),
+        "qkv": (4096, 6144), "gu": (4096, 28672), "d": (14336, 4096),
+    },
+    "phi3_medium": {"qkv": (5120, 7680), "o": (5120, 5120), "gu": (5120, 35840), "d": (17920, 5120)},
+    "llama3_70b": {"qkv": (8192, 10240), "o": (8192, 8192), "gu": (8192, 57344), "d": (28672, 8192)},
+}
+
+# Decode-step layer classes per block (the paper's classes qkv, o, gu, d) and blocks.
+MODEL_BLOCKS = {"llama3_8b": 32, "phi3_medium": 40, "llama3_70b": 80}
+
+
+def model_layers(model: str, fused: bool = True):
+    """[(label, d_in, d_out)] for one decoder block."""
+    sh = SHAPES[model]
+    names = ["qkv", "o", "gu", "d"] if fused else ["q", "k", "v", "o", "gate", "up", "down"]
+    return [(n, *sh[n]) for n in names]
+
+
+def layer_seed(*parts) -> int:
+    """Stable 63-bit seed from a tuple of labels (hash(cfg, layer, block/step))."""
+    h = hashlib.sha256("/".join(str(p) for p in parts).encode()).digest()
+    return int.from_bytes(h[:8], "little") & ((1 << 63) - 1)
+
+
+def gen_weight_fp16(d_in: int, d_out: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    col = rng.lognormal(0.0, 0.25, size=d_out)
+    W = rng.normal(0.0, 0.02, size=(d_in, d_out)) * col[None, :]
+    return W.astype(np.float16)
+
+
+def gen_activations(d_in: int, n_steps: int, seed: int, kind: str = "qkv") -> np.ndarray:
+    """[n_steps, d_in] fp16 outlier-heavy decode activations."""
+    rng = np.random.default_rng(seed)
+    sigma = rng.lognormal(0.0, 0.5, size=d_in)
+    outl = rng.choice(d_in, size=min(8, d_in), replace=False)
+    sigma[outl] *= 200.0 if kind in ("d", "down") else 20.0
+    t = rng.standard_t(3.0, size=(n_steps, d_in))
+    x = np.clip(sigma[None, :] * t, -32768.0, 32768.0)
+    return x.astype(np.float16)
+
+
+def gen_special_activations(d_in: int, kind: str, seed: int = 0) -> np.ndarray:
+    """Correctness-only vectors: ties, signed zeros, all-equal, few distinct magnitudes."""
+    rng = np.random.default_rng(seed)
+    if kind == "all_equal":
+        x = np.full(d_in, 1.5)
+        x[rng.random(d_in) < 0.5] *= -1
+    elif kind == "zeros":
+        x = np.zeros(d_in)
+        x[rng.random(d_in) < 0.5] = -0.0
+    elif kind == "ties":
+        x = rng.choice([0.0, -0.0, 0.25, -0.25, 1.0, -1.0, 3.0, -3.0], size=d_in)
+    elif kind == "sparse":
+        x = np.zeros(d_in)
+        nz = rng.choice(d_in, size=max(1, d_in // 64), replace=False)
+        x[nz] = rng.standard_normal(len(nz))
+    else:
+        raise ValueError(kind)
+    return x.astype(np.float16)
+
+
+def gen_perf_layer(d_in: int, d_out: int, bits: int, seed: int, group: int = 128, with_residual: bool = True):
+    """Stored quantities of one quantized layer drawn directly (perf configs 2-5).
+
+    Returns dict q uint8 [d_in, d_out], s fp16 [G, d_out], z uint8 [G, d_out],
+    rc int8 [d_in, d_out] in [-7, 7], rS fp16 [d_out].
+    """
+    rng = np.random.default_rng(seed)
+    G = d_in // group
+    qmax = (1 << bits) - 1
+    q = rng.integers(0, qmax + 1, size=(d_in, d_out), dtype=np.uint8)
+    zlo = 3 if bits == 3 else 7
+    z = rng.integers(zlo, zlo + 2, size=(G, d_out), dtype=np.uint8)
+    s = (0.02 * np.sqrt(12.0) / (1 << bits) * rng.lognormal(0.0, 0.25, size=(G, d_out))).astype(np.float16)
+    out = dict(q=q, s=s, z=z)
+    if with_residual:
+        out["rc"] = rng.integers(-7, 8, size=(d_in, d_out), dtype=np.int8)
+        out["rS"] = (np.median(s.astype(np.float64), axis=0) / 14.0).astype(np.float16)
+    return out
