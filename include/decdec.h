@@ -1,0 +1,161 @@
+/*
+ * decdec.h -- C ABI of the B200-native DecDEC decode hot path.
+ *
+ * DecDEC (arXiv 2412.20185) augments every decode-step linear layer (a GEMV) with
+ * dynamic error compensation:
+ *
+ *     o = W_hat x + sum_{i in S(x)} x_i * R_hat[i, :]
+ *
+ *   (1) S(x) = indices of the k largest |x_i|                     (P:207 step 1, "Exact")
+ *   (2) fetch R_hat[S, :] (4-bit residual codes + per-column scales) from pinned host
+ *       memory with GPU zero-copy loads over PCIe                  (P:207 step 2)
+ *   (3) o_dec = x[S]^T R_hat[S, :]                                 (P:207 step 3)
+ *   (4) o = o_b + o_dec, o_b = W_hat x the base GEMV               (P:207 step 4)
+ *
+ * Conventions (all entry points):
+ *   - Pointers are plain device / host pointers; no framework types.  "device" means
+ *     CUDA global memory of the current device; "host mapped" means memory returned by
+ *     decdec_host_alloc (or cudaHostAlloc(..., cudaHostAllocMapped)).
+ *   - Ownership: the caller owns every buffer.  The library never allocates on the hot
+ *     path.  The workspace is caller-provided, reusable across layers, one per
+ *     concurrently used stream, and must be zeroed once (decdec_workspace_init) before
+ *     its first use; every successful call leaves it ready for the next call.
+ *   - Errors: arguments are validated synchronously; on error nothing is enqueued and a
+ *     negative decdec_status is returned.  Launch failures return DECDEC_ECUDA.
+ *     Asynchronous device faults surface at the next stream synchronisation.
+ *   - fp16 values are passed as uint16_t bit patterns (IEEE binary16).
+ *   - Shapes: d_in % 128 == 0 (group size 128), 128 <= d_in <= 32768,
+ *     d_out % 32 == 0 (16-byte residual rows), d_out >= 32.
+ *   - Determinism: results are bit-identical run to run (no value atomics; fixed
+ *     accumulation orders).
+ */
+#ifndef DECDEC_H_
+#define DECDEC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* decdec_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  DECDEC_OK = 0,
+  DECDEC_EINVAL = -1,       /* bad shape / k / chunk / null pointer                        */
+  DECDEC_EALIGN = -2,       /* pointer not 16-byte aligned                                */
+  DECDEC_ENOTMAPPED = -3,   /* residual pointer is not host-mapped (zero-copy) memory      */
+  DECDEC_EUNSUPPORTED = -4, /* bits / r_bits / d_in outside the supported set              */
+  DECDEC_ECUDA = -5,        /* CUDA runtime error (allocation, launch, attribute)          */
+  DECDEC_ENCCL = -6,        /* reserved for the library-owned communicator path            */
+  DECDEC_ESPACE = -7        /* workspace or output buffer too small                        */
+} decdec_status;
+
+#define DECDEC_GROUP 128
+
+/*
+ * One quantized linear layer (or this rank's output-column shard of one).
+ *
+ * Base weights W_hat = s * (q - z), RTN asymmetric, groups of 128 input channels per
+ * output column (DESIGN.md ledger L5; stands in for AWQ).  Packed K-major:
+ * output column j is a contiguous row of its d_in codes (ledger L6):
+ *   w_bits = 4 (layout W4K): uint32 [d_out][d_in/8]; channel c of an 8-channel word at
+ *            bit 4*(c>>1) + 16*(c&1).
+ *   w_bits = 3 (layout W3K): uint32 [d_out][3*d_in/32]; per 32-channel slice 3 words:
+ *            channel c < 30 -> word c/10, bits 16*h + 3*p .. +2 with r = c%10, p = r/2,
+ *            h = r%2; channels 30/31 -> code bit b at word b, bit 15 (+16 for c = 31).
+ *            3.0 bits per weight.
+ * Residual R_hat = S_j * c_ij, c in [-7, 7]: rows = input channels,
+ * contiguous, in HOST MAPPED memory (zero-copy):
+ *   r_bits = 4  (layout Rq):  uint32 [d_in][d_out/8], nibble = c + 8, column c of an
+ *            8-column word at bit 4*(c>>1) + 16*(c&1); r_scales fp16 [d_out] (host mapped,
+ *            fetched on every call).
+ *   r_bits = 16 (layout R16): fp16 [d_in][d_out] (Table 3 "FP16"); r_scales NULL.
+ */
+typedef struct decdec_layer {
+  int32_t d_in, d_out;       /* d_out = this rank's shard width when sharded             */
+  int32_t w_bits;            /* 3 | 4                                                    */
+  int32_t group_size;        /* must be 128                                              */
+  const void* w_packed;      /* device, 16-B aligned, W3K | W4K                           */
+  const uint16_t* w_scales;  /* device fp16 [d_out][d_in/128], 16-B aligned               */
+  const uint8_t* w_zeros;    /* device u8   [d_out][d_in/128], 16-B aligned               */
+  int32_t r_bits;            /* 4 (paper default) | 16                                   */
+  const void* r_rows;        /* HOST mapped, 16-B aligned, Rq | R16                       */
+  const uint16_t* r_scales;  /* HOST mapped fp16 [d_out] (r_bits = 4) | NULL (r_bits = 16) */
+} decdec_layer;
+
+/* Bytes of workspace for layers with k <= max_k and d_out <= max_d_out: the paper's
+ * k x (4+2) B sc_indices/x[sc_indices] buffer plus fp32 partial outputs and
+ * per-256-column arrival counters used by the deterministic combine. */
+size_t decdec_workspace_bytes(int32_t max_k, int32_t max_d_out);
+
+/* Zero a workspace (stream-ordered).  Required once before first use. */
+decdec_status decdec_workspace_init(void* ws, size_t ws_bytes, decdec_stream_t stream);
+
+/*
+ * decdec_linear: y = fp16_rn( W_hat x + sum_{i in S} x_i R_hat[i,:] ), one decode step
+ * of one layer.  x, y: device fp16 [d_in] / [d_out], 16-B aligned.
+ *   chunk = 0    : S = exact global Top-k of |x| ("Exact"); 0 <= k <= d_in.
+ *   chunk = 1024 : the paper's chunk partition made exact and deterministic:
+ *                  in every contiguous 1024-channel chunk the top min(k, len) channels,
+ *                  here k = k_chunk <= 1024 (total = sum over chunks).
+ *   Magnitude = 15-bit key bits(x) & 0x7FFF; ties -> lower index (ledger L2).  x must be
+ *   finite (NaN/Inf: undefined).
+ *   k = 0 runs the plain quantized GEMV, bit-identical to decdec_gemv.
+ *   sel: optional device int32 output receiving the selected indices ascending
+ *        (S:119); capacity >= total selected.  May be NULL.
+ * Enqueues on `stream`; asynchronous.
+ */
+decdec_status decdec_linear(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk,
+                            uint16_t* y, int32_t* sel, void* ws, size_t ws_bytes,
+                            decdec_stream_t stream);
+
+/* Plain quantized GEMV y = fp16_rn(W_hat x) (the uncompensated baseline, k = 0). */
+decdec_status decdec_gemv(const decdec_layer* L, const uint16_t* x, uint16_t* y, void* ws,
+                          size_t ws_bytes, decdec_stream_t stream);
+
+/* Step (1) alone: exact Top-k (S:117-131 exact_topk).  idx: device int32 [n_sel],
+ * xs: device fp16 [n_sel]; n_sel = k (chunk = 0) or sum_c min(k, len_c) (chunk > 0). */
+decdec_status decdec_select(const uint16_t* x, int32_t d_in, int32_t k, int32_t chunk,
+                            int32_t* idx, uint16_t* xs, decdec_stream_t stream);
+
+/* Number of channels selected for (d_in, k, chunk); -1 on invalid arguments. */
+int32_t decdec_num_selected(int32_t d_in, int32_t k, int32_t chunk);
+
+/* ------------------------------------------------------------------ offline, host-only */
+/* Pack base codes q (u8 [d_in][d_out], logical W layout, values < 2^bits) into W3K/W4K
+ * (uint32 [d_out][d_in*bits/32]).  out_bytes must be >= d_out*d_in*bits/8. */
+decdec_status decdec_pack_weights(const uint8_t* q, int32_t d_in, int32_t d_out, int32_t bits,
+                                  void* out, size_t out_bytes);
+
+/* Pack residual codes c (int8 [d_in][d_out], values in [-7, 7]) into Rq
+ * (uint32 [d_in][d_out/8]).  out_bytes >= d_in*d_out/2. */
+decdec_status decdec_pack_residual(const int8_t* c, int32_t d_in, int32_t d_out, void* out,
+                                   size_t out_bytes);
+
+/* Pinned, device-mapped host memory for the residual store (zero-copy source).
+ * numa_node >= 0 binds the pages to that node before pinning; -1 = no binding.
+ * write_combined != 0 requests write-combined pages (GPU reads only). */
+decdec_status decdec_host_alloc(size_t bytes, int32_t numa_node, int32_t write_combined, void** p);
+void decdec_host_free(void* p);
+
+/* ------------------------------------------------------------------ debug / introspection */
+/* Decode the packed weights with the GEMV kernel's own in-register decode path and write
+ * the integer codes to q_out (device u8 [d_out][d_in]).  For bit-exact layout tests. */
+decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out,
+                                          decdec_stream_t stream);
+
+/* Launch plan chosen for a layer (tile rows, consumer warps, stages, grid) as text. */
+decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, size_t buf_bytes);
+
+/* Number of kernels decdec_linear enqueues for (k): 2 when k > 0 (select + fused), else 1. */
+int32_t decdec_launches_per_call(int32_t k);
+
+const char* decdec_status_string(decdec_status s);
+const char* decdec_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DECDEC_H_ */

@@ -1,0 +1,30 @@
+"""B200-native DecDEC decode hot path (arXiv 2412.20185).
+
+    o = W_hat x + sum_{i in TopK(|x|)} x_i R_hat[i, :]
+
+The compute lives in libdecdec.so (hand-written sm_100a CUDA behind the C ABI of
+include/decdec.h); this package is the thin binding plus buffer ownership.
+"""
+
+from ._lib import (  # noqa: F401
+    EXPORTED,
+    LIB_PATH,
+    DecdecError,
+    decdec_debug_unpack_weights,
+    decdec_gemv,
+    decdec_host_alloc,
+    decdec_host_free,
+    decdec_launches_per_call,
+    decdec_layer,
+    decdec_linear,
+    decdec_num_selected,
+    decdec_pack_residual,
+    decdec_pack_weights,
+    decdec_plan_string,
+    decdec_select,
+    decdec_status_string,
+    decdec_version,
+    decdec_workspace_bytes,
+    decdec_workspace_init,
+)
+from .layer import HostBuffer, QuantLinear, Workspace, pack_residual_into, pack_weights, select  # noqa: F401

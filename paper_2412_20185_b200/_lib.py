@@ -1,0 +1,147 @@
+"""Thin ctypes binding of libdecdec.so (include/decdec.h).  Argument marshalling only:
+every step of the hot path runs in the library's sm_100a kernels.  There is no CPU or
+PyTorch fallback: if the library is missing this module raises at import."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdecdec.so")
+
+DECDEC_OK = 0
+STATUS = {0: "DECDEC_OK", -1: "DECDEC_EINVAL", -2: "DECDEC_EALIGN", -3: "DECDEC_ENOTMAPPED",
+          -4: "DECDEC_EUNSUPPORTED", -5: "DECDEC_ECUDA", -6: "DECDEC_ENCCL", -7: "DECDEC_ESPACE"}
+
+
+class DecdecError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: {STATUS.get(status, status)} ({_lib.decdec_status_string(status).decode()})")
+        self.status = status
+
+
+class decdec_layer(ctypes.Structure):
+    _fields_ = [
+        ("d_in", ctypes.c_int32), ("d_out", ctypes.c_int32),
+        ("w_bits", ctypes.c_int32), ("group_size", ctypes.c_int32),
+        ("w_packed", ctypes.c_void_p), ("w_scales", ctypes.c_void_p), ("w_zeros", ctypes.c_void_p),
+        ("r_bits", ctypes.c_int32),
+        ("r_rows", ctypes.c_void_p), ("r_scales", ctypes.c_void_p),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"libdecdec.so not found at {LIB_PATH}: build it with `python -m paper_2412_20185_b200.build` "
+            "(no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, SZ, VP = ctypes.POINTER, ctypes.c_int32, ctypes.c_size_t, ctypes.c_void_p
+    Lp = P(decdec_layer)
+    sig = {
+        "decdec_workspace_bytes": (SZ, [I32, I32]),
+        "decdec_workspace_init": (I32, [VP, SZ, VP]),
+        "decdec_linear": (I32, [Lp, VP, I32, I32, VP, VP, VP, SZ, VP]),
+        "decdec_gemv": (I32, [Lp, VP, VP, VP, SZ, VP]),
+        "decdec_select": (I32, [VP, I32, I32, I32, VP, VP, VP]),
+        "decdec_num_selected": (I32, [I32, I32, I32]),
+        "decdec_pack_weights": (I32, [VP, I32, I32, I32, VP, SZ]),
+        "decdec_pack_residual": (I32, [VP, I32, I32, VP, SZ]),
+        "decdec_host_alloc": (I32, [SZ, I32, I32, P(VP)]),
+        "decdec_host_free": (None, [VP]),
+        "decdec_debug_unpack_weights": (I32, [Lp, VP, VP]),
+        "decdec_plan_string": (I32, [Lp, I32, ctypes.c_char_p, SZ]),
+        "decdec_launches_per_call": (I32, [I32]),
+        "decdec_status_string": (ctypes.c_char_p, [I32]),
+        "decdec_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTED = [
+    "decdec_workspace_bytes", "decdec_workspace_init", "decdec_linear", "decdec_gemv", "decdec_select",
+    "decdec_num_selected", "decdec_pack_weights", "decdec_pack_residual", "decdec_host_alloc",
+    "decdec_host_free", "decdec_debug_unpack_weights", "decdec_plan_string", "decdec_launches_per_call",
+    "decdec_status_string", "decdec_version",
+]
+
+
+def _check(status: int, where: str):
+    if status != DECDEC_OK:
+        raise DecdecError(status, where)
+
+
+def _vp(p):
+    return ctypes.c_void_p(int(p) if p else 0)
+
+
+# ------------------------------------------------------------------ same names as the C ABI
+def decdec_workspace_bytes(max_k: int, max_d_out: int) -> int:
+    return int(_lib.decdec_workspace_bytes(max_k, max_d_out))
+
+
+def decdec_workspace_init(ws, ws_bytes, stream=0):
+    _check(_lib.decdec_workspace_init(_vp(ws), ws_bytes, _vp(stream)), "decdec_workspace_init")
+
+
+def decdec_linear(L: decdec_layer, x, k: int, chunk: int, y, sel, ws, ws_bytes: int, stream=0):
+    _check(_lib.decdec_linear(ctypes.byref(L), _vp(x), k, chunk, _vp(y), _vp(sel), _vp(ws), ws_bytes, _vp(stream)),
+           "decdec_linear")
+
+
+def decdec_gemv(L: decdec_layer, x, y, ws=0, ws_bytes=0, stream=0):
+    _check(_lib.decdec_gemv(ctypes.byref(L), _vp(x), _vp(y), _vp(ws), ws_bytes, _vp(stream)), "decdec_gemv")
+
+
+def decdec_select(x, d_in: int, k: int, chunk: int, idx, xs, stream=0):
+    _check(_lib.decdec_select(_vp(x), d_in, k, chunk, _vp(idx), _vp(xs), _vp(stream)), "decdec_select")
+
+
+def decdec_num_selected(d_in: int, k: int, chunk: int) -> int:
+    return int(_lib.decdec_num_selected(d_in, k, chunk))
+
+
+def decdec_pack_weights(q_ptr, d_in, d_out, bits, out_ptr, out_bytes):
+    _check(_lib.decdec_pack_weights(_vp(q_ptr), d_in, d_out, bits, _vp(out_ptr), out_bytes), "decdec_pack_weights")
+
+
+def decdec_pack_residual(c_ptr, d_in, d_out, out_ptr, out_bytes):
+    _check(_lib.decdec_pack_residual(_vp(c_ptr), d_in, d_out, _vp(out_ptr), out_bytes), "decdec_pack_residual")
+
+
+def decdec_host_alloc(nbytes: int, numa_node: int = -1, write_combined: int = 0) -> int:
+    p = ctypes.c_void_p()
+    _check(_lib.decdec_host_alloc(nbytes, numa_node, write_combined, ctypes.byref(p)), "decdec_host_alloc")
+    return int(p.value)
+
+
+def decdec_host_free(p):
+    _lib.decdec_host_free(_vp(p))
+
+
+def decdec_debug_unpack_weights(L: decdec_layer, q_out, stream=0):
+    _check(_lib.decdec_debug_unpack_weights(ctypes.byref(L), _vp(q_out), _vp(stream)), "decdec_debug_unpack_weights")
+
+
+def decdec_plan_string(L: decdec_layer, k_sel: int) -> str:
+    buf = ctypes.create_string_buffer(512)
+    _check(_lib.decdec_plan_string(ctypes.byref(L), k_sel, buf, 512), "decdec_plan_string")
+    return buf.value.decode()
+
+
+def decdec_launches_per_call(k: int) -> int:
+    return int(_lib.decdec_launches_per_call(k))
+
+
+def decdec_status_string(s: int) -> str:
+    return _lib.decdec_status_string(s).decode()
+
+
+def decdec_version() -> str:
+    return _lib.decdec_version().decode()

@@ -1,0 +1,330 @@
+// C-ABI entry points of libdecdec (include/decdec.h): validation, launch planning and
+// launches of the sm_100a kernels in select.cuh / linear.cuh.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "decdec.h"
+#include "linear.cuh"
+#include "select.cuh"
+
+using namespace decdec;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
+
+int device_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int gcd(int a, int b) { while (b) { int t = a % b; a = b; b = t; } return a; }
+
+struct Plan {
+  int G, RP, RPT, TR, NC, stages, n_tiles, grid, NGW;
+  uint32_t stage_bytes, off_s, off_z;
+  size_t smem;
+};
+
+constexpr size_t kSmemBudget = 200 * 1024;
+
+decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl) {
+  Plan p{};
+  p.G = d_in / DECDEC_GROUP;
+  const int sms = device_sms();
+  p.RP = 1;
+  while (p.RP * 2 * p.G <= 384) p.RP *= 2;  // <= 12 consumer warps
+  while (p.RP > 1 && (d_out / p.RP < sms || d_out % p.RP)) p.RP /= 2;
+  const int unit = 16 / gcd(p.G, 16);  // TR * G % 16 == 0 for the zeros bulk copy
+  p.RPT = 1;
+  while ((p.RP * p.RPT) % unit) p.RPT *= 2;
+  p.TR = p.RP * p.RPT;
+  if (d_out % p.TR || kSegCols % p.TR) return DECDEC_EUNSUPPORTED;
+  p.NC = (p.RP * p.G + 31) / 32;
+  if (p.NC > 12) return DECDEC_EUNSUPPORTED;
+  const uint32_t row_bytes = (uint32_t)d_in * bits / 8;
+  p.off_s = (uint32_t)p.TR * row_bytes;
+  p.off_z = p.off_s + (uint32_t)p.TR * p.G * 2;
+  p.stage_bytes = (uint32_t)align_up(p.off_z + (uint32_t)p.TR * p.G, 16);
+  const size_t red = (size_t)2 * p.TR * p.G * 4;
+  const size_t avail = kSmemBudget - red - 16 * 8;
+  p.stages = (int)(avail / p.stage_bytes);
+  if (p.stages > 8) p.stages = 8;
+  if (p.stages < 2) return DECDEC_EUNSUPPORTED;
+  p.n_tiles = d_out / p.TR;
+  p.grid = p.n_tiles < sms ? p.n_tiles : sms;
+  p.NGW = k_sel > 0 ? 2 : 0;
+  p.smem = (size_t)p.stages * p.stage_bytes + red + (size_t)2 * p.stages * 8;
+  *pl = p;
+  return DECDEC_OK;
+}
+
+struct WsLayout {
+  size_t cnt, idx, xs, ob, sdev, part, total;
+};
+WsLayout ws_layout(int k, int d_out) {
+  WsLayout w{};
+  w.cnt = 0;
+  w.idx = align_up((size_t)kCntSlots * 4);
+  w.xs = w.idx + align_up((size_t)k * 4);
+  w.ob = w.xs + align_up((size_t)k * 2);
+  w.sdev = w.ob + align_up((size_t)d_out * 4);
+  w.part = w.sdev + align_up((size_t)d_out * 2);
+  const size_t n_rb = ((size_t)k + kRB - 1) / kRB;
+  w.total = w.part + align_up(n_rb * d_out * 4);
+  return w;
+}
+
+decdec_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return DECDEC_OK;
+  fprintf(stderr, "[decdec] CUDA error: %s\n", cudaGetErrorString(e));
+  return DECDEC_ECUDA;
+}
+
+template <typename K>
+decdec_status set_smem_attr(K kern, size_t bytes) {
+  return cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+std::once_flag g_attr_once;
+decdec_status g_attr_status = DECDEC_OK;
+void init_attrs() {
+  decdec_status s = DECDEC_OK;
+  const size_t lin = 227 * 1024;
+  if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 4>, lin);
+  if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4>, lin);
+  if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 16>, lin);
+  if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 16>, lin);
+  if (s == DECDEC_OK) s = set_smem_attr(k_select<1024>, 64 * 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_select<256>, 64 * 1024);
+  g_attr_status = s;
+}
+decdec_status ensure_attrs() {
+  std::call_once(g_attr_once, init_attrs);
+  return g_attr_status;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+bool is_host_mapped(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+}
+
+decdec_status check_layer(const decdec_layer* L, bool need_residual) {
+  if (!L) return DECDEC_EINVAL;
+  if (L->group_size != DECDEC_GROUP) return DECDEC_EUNSUPPORTED;
+  if (L->w_bits != 3 && L->w_bits != 4) return DECDEC_EUNSUPPORTED;
+  if (L->d_in < 128 || L->d_in > 32768 || L->d_in % DECDEC_GROUP) return DECDEC_EINVAL;
+  if (L->d_out < 32 || L->d_out % 32) return DECDEC_EINVAL;
+  if (!L->w_packed || !L->w_scales || !L->w_zeros) return DECDEC_EINVAL;
+  if (!aligned16(L->w_packed) || !aligned16(L->w_scales) || !aligned16(L->w_zeros)) return DECDEC_EALIGN;
+  if (!is_device_ptr(L->w_packed) || !is_device_ptr(L->w_scales) || !is_device_ptr(L->w_zeros)) return DECDEC_EINVAL;
+  if (need_residual) {
+    if (L->r_bits != 4 && L->r_bits != 16) return DECDEC_EUNSUPPORTED;
+    if (!L->r_rows || (L->r_bits == 4 && !L->r_scales)) return DECDEC_EINVAL;
+    if (!aligned16(L->r_rows) || (L->r_bits == 4 && !aligned16(L->r_scales))) return DECDEC_EALIGN;
+    if (!is_host_mapped(L->r_rows) || (L->r_bits == 4 && !is_host_mapped(L->r_scales))) return DECDEC_ENOTMAPPED;
+  }
+  return DECDEC_OK;
+}
+
+int n_selected(int d_in, int k, int chunk) {
+  if (k < 0 || d_in <= 0) return -1;
+  if (chunk == 0) return k <= d_in ? k : -1;
+  if (chunk < 32 || chunk > 32768 || k > chunk) return -1;
+  const int full = d_in / chunk, rem = d_in % chunk;
+  return full * k + (rem < k ? rem : k);
+}
+
+decdec_status launch_select(const uint16_t* x, int d_in, int k, int chunk, int* idx, uint16_t* xs, int* sel,
+                            cudaStream_t st) {
+  if (chunk == 0) {
+    k_select<1024><<<1, 1024, (size_t)d_in * 2, st>>>(x, d_in, k, 0, idx, xs, sel);
+  } else {
+    const int nseg = (d_in + chunk - 1) / chunk;
+    if (chunk <= 4096)
+      k_select<256><<<nseg, 256, (size_t)chunk * 2, st>>>(x, d_in, k, chunk, idx, xs, sel);
+    else
+      k_select<1024><<<nseg, 1024, (size_t)chunk * 2, st>>>(x, d_in, k, chunk, idx, xs, sel);
+  }
+  return cuda_status(cudaGetLastError());
+}
+
+template <int BITS, int RBITS>
+decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(32 * (1 + pl.NC + pl.NGW));
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cuda_status(cudaLaunchKernelEx(&cfg, k_linear<BITS, RBITS>, p));
+}
+
+decdec_status launch_linear(const LinearParams& p, const Plan& pl, int bits, int rbits, bool pdl, cudaStream_t st) {
+  if (bits == 3) return rbits == 16 ? launch_linear_t<3, 16>(p, pl, pdl, st) : launch_linear_t<3, 4>(p, pl, pdl, st);
+  return rbits == 16 ? launch_linear_t<4, 16>(p, pl, pdl, st) : launch_linear_t<4, 4>(p, pl, pdl, st);
+}
+
+LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, const Plan& pl) {
+  LinearParams p{};
+  p.w = static_cast<const uint8_t*>(L->w_packed);
+  p.ws = L->w_scales;
+  p.wz = L->w_zeros;
+  p.x = x;
+  p.y = y;
+  p.d_in = L->d_in;
+  p.d_out = L->d_out;
+  p.G = pl.G;
+  p.row_bytes = L->d_in * L->w_bits / 8;
+  p.TR = pl.TR;
+  p.RP = pl.RP;
+  p.RPT = pl.RPT;
+  p.NC = pl.NC;
+  p.stages = pl.stages;
+  p.n_tiles = pl.n_tiles;
+  p.stage_bytes = pl.stage_bytes;
+  p.off_s = pl.off_s;
+  p.off_z = pl.off_z;
+  p.NGW = pl.NGW;
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t decdec_workspace_bytes(int32_t max_k, int32_t max_d_out) {
+  if (max_k < 0 || max_d_out < 0) return 0;
+  return ws_layout(max_k, max_d_out).total;
+}
+
+decdec_status decdec_workspace_init(void* ws, size_t ws_bytes, decdec_stream_t stream) {
+  if (!ws || ws_bytes < (size_t)kCntSlots * 4) return DECDEC_EINVAL;
+  return cuda_status(cudaMemsetAsync(ws, 0, ws_bytes, (cudaStream_t)stream));
+}
+
+int32_t decdec_num_selected(int32_t d_in, int32_t k, int32_t chunk) { return n_selected(d_in, k, chunk); }
+
+decdec_status decdec_select(const uint16_t* x, int32_t d_in, int32_t k, int32_t chunk, int32_t* idx, uint16_t* xs,
+                            decdec_stream_t stream) {
+  if (!x || !idx || !xs) return DECDEC_EINVAL;
+  if (d_in <= 0 || d_in > 32768) return DECDEC_EINVAL;
+  if (n_selected(d_in, k, chunk) < 0) return DECDEC_EINVAL;
+  decdec_status s = ensure_attrs();
+  if (s != DECDEC_OK) return s;
+  if (k == 0) return DECDEC_OK;
+  return launch_select(x, d_in, k, chunk, idx, xs, nullptr, (cudaStream_t)stream);
+}
+
+decdec_status decdec_gemv(const decdec_layer* L, const uint16_t* x, uint16_t* y, void* ws, size_t ws_bytes,
+                          decdec_stream_t stream) {
+  (void)ws;
+  (void)ws_bytes;
+  decdec_status s = check_layer(L, false);
+  if (s != DECDEC_OK) return s;
+  if (!x || !y) return DECDEC_EINVAL;
+  if (!aligned16(x) || !aligned16(y)) return DECDEC_EALIGN;
+  if ((s = ensure_attrs()) != DECDEC_OK) return s;
+  Plan pl;
+  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, 0, &pl)) != DECDEC_OK) return s;
+  LinearParams p = base_params(L, x, y, pl);
+  return launch_linear(p, pl, L->w_bits, 4, false, (cudaStream_t)stream);
+}
+
+decdec_status decdec_linear(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk, uint16_t* y,
+                            int32_t* sel, void* ws, size_t ws_bytes, decdec_stream_t stream) {
+  decdec_status s = check_layer(L, k > 0);
+  if (s != DECDEC_OK) return s;
+  if (!x || !y) return DECDEC_EINVAL;
+  if (!aligned16(x) || !aligned16(y)) return DECDEC_EALIGN;
+  const int k_sel = n_selected(L->d_in, k, chunk);
+  if (k_sel < 0) return DECDEC_EINVAL;
+  if ((s = ensure_attrs()) != DECDEC_OK) return s;
+  Plan pl;
+  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &pl)) != DECDEC_OK) return s;
+  LinearParams p = base_params(L, x, y, pl);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k_sel == 0) return launch_linear(p, pl, L->w_bits, 4, false, st);
+
+  if (!ws) return DECDEC_EINVAL;
+  const WsLayout wl = ws_layout(k_sel, L->d_out);
+  if (wl.total > ws_bytes) return DECDEC_ESPACE;
+  if (!aligned16(ws)) return DECDEC_EALIGN;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  p.k_sel = k_sel;
+  p.idx = reinterpret_cast<const int*>(base + wl.idx);
+  p.xs = reinterpret_cast<const uint16_t*>(base + wl.xs);
+  p.r_rows = static_cast<const uint8_t*>(L->r_rows);
+  p.r_scales = L->r_scales;
+  p.r_row_bytes = L->d_out * L->r_bits / 8;
+  p.ob = reinterpret_cast<float*>(base + wl.ob);
+  p.part = reinterpret_cast<float*>(base + wl.part);
+  p.sdev = reinterpret_cast<uint16_t*>(base + wl.sdev);
+  p.cnt = reinterpret_cast<uint32_t*>(base + wl.cnt);
+  p.n_seg = (L->d_out + kSegCols - 1) / kSegCols;
+  if (p.n_seg > kCntSlots) return DECDEC_EUNSUPPORTED;
+  p.n_rb = (k_sel + kRB - 1) / kRB;
+  p.n_items = p.n_seg * p.n_rb;
+  if ((s = launch_select(x, L->d_in, k, chunk, reinterpret_cast<int*>(base + wl.idx),
+                         reinterpret_cast<uint16_t*>(base + wl.xs), sel, st)) != DECDEC_OK)
+    return s;
+  return launch_linear(p, pl, L->w_bits, L->r_bits, true, st);
+}
+
+decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out, decdec_stream_t stream) {
+  decdec_status s = check_layer(L, false);
+  if (s != DECDEC_OK) return s;
+  if (!q_out) return DECDEC_EINVAL;
+  const int blocks = 4 * device_sms();
+  if (L->w_bits == 3)
+    k_debug_unpack<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint8_t*>(L->w_packed), L->d_in, L->d_out, q_out);
+  else
+    k_debug_unpack<4><<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint8_t*>(L->w_packed), L->d_in, L->d_out, q_out);
+  return cuda_status(cudaGetLastError());
+}
+
+decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, size_t buf_bytes) {
+  if (!L || !buf) return DECDEC_EINVAL;
+  const int k_sel = k;  // caller passes the selected count
+  Plan pl;
+  decdec_status s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &pl);
+  if (s != DECDEC_OK) return s;
+  snprintf(buf, buf_bytes,
+           "{\"G\": %d, \"RP\": %d, \"RPT\": %d, \"TR\": %d, \"NC\": %d, \"NGW\": %d, \"stages\": %d, "
+           "\"stage_bytes\": %u, \"n_tiles\": %d, \"grid\": %d, \"threads\": %d, \"smem\": %zu}",
+           pl.G, pl.RP, pl.RPT, pl.TR, pl.NC, pl.NGW, pl.stages, pl.stage_bytes, pl.n_tiles, pl.grid,
+           32 * (1 + pl.NC + pl.NGW), pl.smem);
+  return DECDEC_OK;
+}
+
+int32_t decdec_launches_per_call(int32_t k) { return k > 0 ? 2 : 1; }
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// In-register decode of the packed layouts of include/decdec.h (DESIGN.md ledger L6).
+//
+// Base weights: a code q is masked in place into the mantissa field of an fp16 half,
+// exponent 0, i.e. the fp16 SUBNORMAL q * 2^(pos-24) where pos = its bit offset inside
+// the half.  One LOP3 extracts two codes (one per half); FHFMA multiplies them exactly
+// by x.  Codes at different offsets feed different fp32 accumulators ("scale classes")
+// that are recombined once per group with exact power-of-two factors.
+//   W4K: class 0 = offset 0 (x 2^-24), class 1 = offset 4 (x 2^-20)
+//   W3K: class 0 = offset 0 (x 2^-24), class 1 = offset 3 (x 2^-21), class 2 = offset 6 (x 2^-18)
+// The group sum is  sum q*x = 2^24 * (acc0 + acc1/16)            (4-bit)
+//                             2^24 * (acc0 + acc1/8 + acc2/64)    (3-bit)
+#pragma once
+#include <cstdint>
+#include "ptx.cuh"
+
+namespace decdec {
+
+// ---------------------------------------------------------------- W4K
+// word: channels c = 0..7 at bit 4*(c>>1) + 16*(c&1); pair p = channels (2p, 2p+1).
+// m[p] holds the pair as two subnormal halves; class(p) = p & 1.
+__device__ __forceinline__ void decode_w4_word(uint32_t w, uint32_t m[4]) {
+  m[0] = w & 0x000F000Fu;
+  m[1] = w & 0x00F000F0u;
+  const uint32_t v = w >> 8;
+  m[2] = v & 0x000F000Fu;
+  m[3] = v & 0x00F000F0u;
+}
+__host__ __device__ constexpr int w4_class(int p) { return p & 1; }
+
+// acc[0..1] += codes(w) . x(xr[0..3]) for one 8-channel word; xr[p] = (x[2p], x[2p+1]).
+__device__ __forceinline__ void fma_w4_word(uint32_t w, const uint32_t* xr, float* acc) {
+  uint32_t m[4];
+  decode_w4_word(w, m);
+  acc[0] = fhfma2(m[0], xr[0], acc[0]);
+  acc[1] = fhfma2(m[1], xr[1], acc[1]);
+  acc[0] = fhfma2(m[2], xr[2], acc[0]);
+  acc[1] = fhfma2(m[3], xr[3], acc[1]);
+}
+
+// ---------------------------------------------------------------- W3K
+// One 32-channel slice = 3 words.  Pair k = 5t + p (t = word, p = position 0..4) holds
+// channels (10t + 2p, 10t + 2p + 1); pair 15 holds channels (30, 31) assembled from the
+// spare bit 15 / 31 of the three words.  class: p in {0,3} -> 0, p in {1,4} -> 1, p = 2 -> 2,
+// pair 15 -> 2.
+__device__ __forceinline__ void decode_w3_slice(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t m[16]) {
+  const uint32_t w[3] = {w0, w1, w2};
+  uint32_t v[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    m[5 * t + 0] = w[t] & 0x00070007u;
+    m[5 * t + 1] = w[t] & 0x00380038u;
+    m[5 * t + 2] = w[t] & 0x01C001C0u;
+    v[t] = w[t] >> 9;
+    m[5 * t + 3] = v[t] & 0x00070007u;
+    m[5 * t + 4] = v[t] & 0x00380038u;
+  }
+  // spare bits now at bit 6 (low half) / 22 (high half) of v[t]; code bit t -> offset 6 + t
+  m[15] = (v[0] & 0x00400040u) | ((v[1] & 0x00400040u) << 1) | ((v[2] & 0x00400040u) << 2);
+}
+__host__ __device__ constexpr int w3_class(int k) {
+  return k == 15 ? 2 : ((k % 5) == 0 || (k % 5) == 3) ? 0 : ((k % 5) == 2 ? 2 : 1);
+}
+
+// acc[0..2] += codes(slice) . x(xr[0..15])
+__device__ __forceinline__ void fma_w3_slice(uint32_t w0, uint32_t w1, uint32_t w2, const uint32_t* xr, float* acc) {
+  uint32_t m[16];
+  decode_w3_slice(w0, w1, w2, m);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[w3_class(k)] = fhfma2(m[k], xr[k], acc[w3_class(k)]);
+}
+
+// ---------------------------------------------------------------- Rq (residual, 4-bit)
+// word: columns c = 0..7 at bit 4*(c>>1) + 16*(c&1), nibble = code + 8.  Returns the four
+// column pairs as exact fp16 integer codes in [-7, 7]: (1024 + n) via the 0x6400 exponent,
+// minus 1032, both exact in fp16.
+__device__ __forceinline__ void decode_rq_word(uint32_t w, uint32_t c[4]) {
+  const __half2 bias = __halves2half2(__ushort_as_half(0x6408), __ushort_as_half(0x6408));  // 1032
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t h = ((w >> (4 * p)) & 0x000F000Fu) | 0x64006400u;
+    __half2 hv = *reinterpret_cast<const __half2*>(&h);
+    hv = __hsub2(hv, bias);
+    c[p] = *reinterpret_cast<const uint32_t*>(&hv);
+  }
+}
+
+}  // namespace decdec

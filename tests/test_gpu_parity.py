@@ -1,0 +1,190 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the float64 oracle.
+
+Bar (BASELINE.json, DESIGN.md ledger L9): selected indices and decoded integer codes
+bit-exact; outputs |y - y*| <= 1e-3 * max(|y*|, 2^-12 A_j, 2^-14)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import decdec_linear_ref, dequantize_base, quantize_base, quantize_residual, residual, tolerance_ok, topk_ref
+from synth import SHAPES, gen_activations, gen_perf_layer, gen_special_activations, gen_weight_fp16, layer_seed
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2412_20185_b200 as dd  # noqa: E402
+
+DEV = "cuda"
+
+
+def to_dev(x16):
+    return torch.from_numpy(np.ascontiguousarray(x16, np.float16)).to(DEV)
+
+
+def check_close(y_gpu, ref, what=""):
+    y = y_gpu.cpu().numpy()
+    ok, err, bound = tolerance_ok(y, ref["y64"], ref["A"])
+    if not ok.all():
+        bad = np.nonzero(~ok)[0][:8]
+        raise AssertionError(f"{what}: {int((~ok).sum())} / {len(ok)} outside tolerance; e.g. cols {bad}, "
+                             f"y={y[bad]}, y*={ref['y64'][bad]}, err={err[bad]}, bound={bound[bad]}")
+
+
+# ------------------------------------------------------------------ decode (integer codes)
+@pytest.mark.parametrize("bits", [3, 4])
+@pytest.mark.parametrize("shape", [(1024, 256), (4096, 512), (14336, 64)])
+def test_debug_unpack_bit_exact(bits, shape):
+    L = gen_perf_layer(*shape, bits, seed=layer_seed("unpack", bits, *shape), with_residual=False)
+    lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], bits)
+    q = lin.debug_unpack().cpu().numpy()
+    assert np.array_equal(q, L["q"].T)
+
+
+# ------------------------------------------------------------------ selection (bit-exact)
+@pytest.mark.parametrize("d_in", [128, 1024, 4096, 5120, 14336, 17920, 28672])
+def test_select_exact(d_in):
+    X = gen_activations(d_in, 3, seed=layer_seed("sel", d_in), kind="down" if d_in > 8192 else "qkv")
+    for x in X:
+        xd = to_dev(x)
+        for k in sorted({0, 1, 7, d_in // 64, d_in // 12, d_in // 2, d_in}):
+            idx, xs = dd.select(xd, k)
+            ridx, rxs = topk_ref(x, k)
+            assert np.array_equal(idx.cpu().numpy(), ridx), (d_in, k)
+            assert np.array_equal(xs.cpu().numpy().view(np.uint16), rxs.view(np.uint16))
+
+
+@pytest.mark.parametrize("kind", ["all_equal", "zeros", "ties", "sparse"])
+def test_select_ties_and_degenerate(kind):
+    for d_in in (1024, 4096, 14336):
+        x = gen_special_activations(d_in, kind, seed=d_in)
+        for k in (1, 3, 100, d_in // 3, d_in - 1):
+            idx, _ = dd.select(to_dev(x), k)
+            assert np.array_equal(idx.cpu().numpy(), topk_ref(x, k)[0]), (kind, d_in, k)
+
+
+@pytest.mark.parametrize("d_in", [1024, 4096, 17920, 28672])
+def test_select_chunk_mode(d_in):
+    x = gen_activations(d_in, 1, seed=layer_seed("chunk", d_in))[0]
+    for kc in (1, 8, 32, 200, 1024):
+        idx, xs = dd.select(to_dev(x), kc, chunk=1024)
+        ridx, _ = topk_ref(x, kc, chunk=1024)
+        assert np.array_equal(idx.cpu().numpy(), ridx), (d_in, kc)
+
+
+# ------------------------------------------------------------------ config 1 full pipeline
+def _config1(bits=3, seed=1):
+    d_in, d_out = SHAPES["config1"]["l"]
+    W = gen_weight_fp16(d_in, d_out, layer_seed("config1", "W", seed))
+    q, s, z = quantize_base(W, bits)
+    R = residual(W, dequantize_base(q, s, z))
+    rc, rS = quantize_residual(R, 4)
+    r16 = quantize_residual(R, 16)
+    return W, q, s, z, rc, rS, r16
+
+
+@pytest.mark.parametrize("bits", [3, 4])
+@pytest.mark.parametrize("r_bits", [4, 16])
+def test_config1_parity(bits, r_bits):
+    W, q, s, z, rc, rS, r16 = _config1(bits)
+    lin = (dd.QuantLinear.from_codes(q, s, z, bits, rc=rc, rS=rS) if r_bits == 4
+           else dd.QuantLinear.from_codes(q, s, z, bits, r16=r16))
+    ws = dd.Workspace(1024, 1024)
+    X = gen_activations(1024, 8, seed=layer_seed("config1", "x"))
+    for x in X:
+        xd = to_dev(x)
+        for k in (0, 1, 16, 100, 1024):
+            sel = torch.full((max(k, 1),), -1, dtype=torch.int32, device=DEV)
+            y = lin(xd, k, sel=sel, workspace=ws)
+            ref = decdec_linear_ref(q, s, z, x, k, rc=rc if r_bits == 4 else None, rS=rS if r_bits == 4 else None,
+                                    r16=r16 if r_bits == 16 else None)
+            if k:
+                assert np.array_equal(sel.cpu().numpy(), ref["idx"])
+            check_close(y, ref, f"config1 bits={bits} r={r_bits} k={k}")
+
+
+def test_k0_bit_identical_to_gemv():
+    W, q, s, z, rc, rS, r16 = _config1(3)
+    lin = dd.QuantLinear.from_codes(q, s, z, 3, rc=rc, rS=rS)
+    x = to_dev(gen_activations(1024, 1, seed=5)[0])
+    ws = dd.Workspace(64, 1024)
+    assert torch.equal(lin(x, 0, workspace=ws), lin.gemv(x))
+
+
+def test_full_fp16_compensation_recovers_Wx():
+    W, q, s, z, rc, rS, r16 = _config1(3)
+    lin = dd.QuantLinear.from_codes(q, s, z, 3, r16=r16)
+    ws = dd.Workspace(1024, 1024)
+    x = gen_activations(1024, 1, seed=6)[0]
+    y = lin(to_dev(x), 1024, workspace=ws).cpu().numpy()
+    Wx = x.astype(np.float64) @ W.astype(np.float64)
+    A = np.abs(x.astype(np.float64)) @ np.abs(W.astype(np.float64))
+    # fp16 residual rounding (2^-11 relative per element) adds to the L9 bound here
+    err = np.abs(y.astype(np.float64) - Wx)
+    assert np.all(err <= 1e-3 * np.maximum(np.abs(Wx), 2.0 ** -12 * A) + 2e-3 * 2.0 ** -11 * A)
+
+
+# ------------------------------------------------------------------ Llama-3-8B shapes (config 2/3)
+@pytest.mark.parametrize("bits", [3, 4])
+@pytest.mark.parametrize("name", ["qkv", "o", "gu", "d", "k"])
+def test_llama_shapes_sampled(bits, name):
+    d_in, d_out = SHAPES["llama3_8b"][name]
+    L = gen_perf_layer(d_in, d_out, bits, seed=layer_seed("llama3_8b", name, bits))
+    lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], bits, rc=L["rc"], rS=L["rS"])
+    ws = dd.Workspace(oracle.k_from_kchunk(82, d_in), d_out)
+    rng = np.random.default_rng(0)
+    cols = np.unique(np.concatenate([rng.choice(d_out, 384, replace=False), [0, d_out - 1]]))
+    X = gen_activations(d_in, 2, seed=layer_seed("llama3_8b", name, "x"), kind="d" if name == "d" else "qkv")
+    for x in X:
+        xd = to_dev(x)
+        for kc in (0, 8, 21, 82):
+            k = oracle.k_from_kchunk(kc, d_in)
+            sel = torch.empty(max(k, 1), dtype=torch.int32, device=DEV)
+            y = lin(xd, k, sel=sel, workspace=ws).cpu().numpy()
+            ref = oracle.decdec_linear_ref_cols(L["q"], L["s"], L["z"], x, k, cols, rc=L["rc"], rS=L["rS"])
+            if k:
+                assert np.array_equal(sel.cpu().numpy(), ref["idx"])
+            ok, err, bound = tolerance_ok(y[cols], ref["y64"], ref["A"])
+            assert ok.all(), (name, bits, kc, err[~ok][:5], bound[~ok][:5])
+
+
+def test_chunk_mode_linear():
+    d_in, d_out = 5120, 640   # Phi-3 o shard at P=8; 5 chunks
+    L = gen_perf_layer(d_in, d_out, 3, seed=11)
+    lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"])
+    ws = dd.Workspace(5 * 64, d_out)
+    x = gen_activations(d_in, 1, seed=12)[0]
+    y = lin(to_dev(x), 21, chunk=1024, workspace=ws).cpu().numpy()
+    ref = decdec_linear_ref(L["q"], L["s"], L["z"], x, 21, chunk=1024, rc=L["rc"], rS=L["rS"])
+    assert tolerance_ok(y, ref["y64"], ref["A"])[0].all()
+
+
+def test_deterministic_repeats():
+    d_in, d_out = SHAPES["llama3_8b"]["qkv"]
+    L = gen_perf_layer(d_in, d_out, 3, seed=21)
+    lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"])
+    ws = dd.Workspace(256, d_out)
+    x = to_dev(gen_activations(d_in, 1, seed=22)[0])
+    y0 = lin(x, 84, workspace=ws).clone()
+    for _ in range(50):
+        assert torch.equal(lin(x, 84, workspace=ws), y0)
+
+
+def test_rejects_unmapped_residual():
+    L = gen_perf_layer(1024, 256, 3, seed=3)
+    lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"])
+    st = lin.struct
+    bad = torch.zeros(1024 * 128, dtype=torch.uint8, device=DEV)   # device memory, not host-mapped
+    st.r_rows = bad.data_ptr()
+    ws = dd.Workspace(16, 256)
+    x = to_dev(gen_activations(1024, 1, seed=1)[0])
+    y = torch.empty(256, dtype=torch.float16, device=DEV)
+    with pytest.raises(dd.DecdecError) as e:
+        dd.decdec_linear(st, x.data_ptr(), 16, 0, y.data_ptr(), 0, ws.ptr, ws.nbytes,
+                         torch.cuda.current_stream().cuda_stream)
+    assert e.value.status == -3
+    with pytest.raises(dd.DecdecError):
+        lin(x, 2000, workspace=ws)
