@@ -1,0 +1,487 @@
+#!/usr/bin/env python
+"""DecDEC decode-step benchmark (BASELINE.json metric: µs per decode linear layer & tokens/s vs
+k_chunk; % of HBM+PCIe roofline), workload BASELINE.json configs[1]: Llama-3-8B decode, all
+q/k/v/o/gate/up/down shapes x 32 blocks, 3-bit W_hat (group 128) + 4-bit residual in pinned host
+memory, exact Top-k per layer per step on outlier-heavy synthetic activations.
+
+A "step" = one decode step's whole linear stack (224 layer calls, each = exact Top-k selector +
+fused GEMV/zero-copy-gather/combine kernel), replayed as one native CUDA graph
+(decdec_stack_*).  Inputs are resident in HBM when the timed region starts; the step streams
+2.8 GB of packed weights (> 126 MB L2), so no L2 flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--kchunk 21] [--sweep 0,8,21]
+  python bench.py --impl reference ...      # the float64 CPU oracle, timed on host cores
+
+N > 1 (torchrun): output-feature tensor parallelism: every rank holds the
+d_out/N column shard of every layer (+ its own host residual slice) and y is assembled with an
+NCCL all-gather after each layer (strong scaling).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import MODEL_BLOCKS, gen_activations, layer_seed, model_layers  # noqa: E402
+
+METRIC = "µs per decode linear layer & tokens/s vs k_chunk; % of HBM+PCIe roofline"
+GROUP = 128
+
+
+def k_of(kc: int, d_in: int) -> int:
+    return (kc * d_in) // 1024  # ledger L3: k = floor(k_chunk * d_in / 1024)
+
+
+def bytes_hbm(d_in, d_out, bits):
+    """Algorithmic HBM bytes of one layer call: packed codes + fp16 s + u8 z + x + y."""
+    return d_in * d_out * bits // 8 + (d_in // GROUP) * d_out * 3 + 2 * d_in + 2 * d_out
+
+
+def bytes_pcie(k, d_out, r_bits=4):
+    """Algorithmic PCIe bytes: k selected residual rows + every residual scale."""
+    return 0 if k == 0 else k * d_out * r_bits // 8 + (2 * d_out if r_bits == 4 else 0)
+
+
+def load_peaks():
+    hbm, src = 6455.3, "MEASURED_PEAKS.json hbm_gbs"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        hbm, src = 6650.0, "fallback B200_PROFILING.md 6.65 TB/s"
+    pcie, psrc = 51.4, "profiles/r01_probe_links.json zero-copy streaming read max"
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_probe_links.json")) as f:
+            pj = json.load(f)
+        pcie = max(c["GBps"] for c in pj["zc"])
+    except Exception:
+        pass
+    return hbm, src, pcie, psrc
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.lines, self.proc = [], None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(gpu_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [v.strip() for v in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------ model
+class Model:
+    """Llama-3-8B (or another model) decode linear stack on this rank."""
+
+    def __init__(self, dd, torch, model, bits, rank, world, n_x_sets, device):
+        self.layers, self.meta = [], []  # meta: (block, name, d_in, d_out_shard)
+        self.hosts = []
+        shapes = model_layers(model, fused=False) if model == "llama3_8b" else model_layers(model, fused=True)
+        self.n_blocks = MODEL_BLOCKS[model]
+        for b in range(self.n_blocks):
+            for name, d_in, d_out in shapes:
+                d_out_r = d_out // world
+                g = __import__("synth").gen_perf_layer_device(d_in, d_out_r, bits, layer_seed(model, b, name, rank),
+                                                              device=device)
+                row_bytes = d_out_r // 2
+                sc_off = (d_in * row_bytes + 255) // 256 * 256
+                hb = dd.HostBuffer(sc_off + 2 * d_out_r)
+                hv = torch.from_numpy(hb.numpy(np.uint8))
+                hv[: d_in * row_bytes].copy_(g["r"].cpu())
+                hv[sc_off: sc_off + 2 * d_out_r].copy_(g["rS"].view(torch.uint8).cpu())
+                del g["r"]
+                lin = dd.QuantLinear.from_device_packed(d_in, d_out_r, bits, g["w"], g["s"], g["z"], host=hb,
+                                                        r_bits=4, host_scales_off=sc_off)
+                self.layers.append(lin)
+                self.meta.append((b, name, d_in, d_out_r))
+                self.hosts.append(hb)
+        # activations: n_x_sets distinct decode steps, one contiguous fp16 arena per set
+        self.x_off = np.cumsum([0] + [m[2] for m in self.meta])
+        self.y_off = np.cumsum([0] + [m[3] for m in self.meta])
+        self.x_host = []
+        for sset in range(n_x_sets):
+            parts = [gen_activations(d_in, 1, seed=layer_seed(model, b, name, "x", sset),
+                                     kind="d" if name in ("down", "d") else "qkv")[0]
+                     for (b, name, d_in, _) in self.meta]
+            self.x_host.append(np.concatenate(parts))
+        self.x_dev = [torch.from_numpy(h).to(device) for h in self.x_host]
+        self.y_dev = torch.empty(int(self.y_off[-1]), dtype=torch.float16, device=device)
+        self.max_d_out = max(m[3] for m in self.meta)
+        self.max_d_in = max(m[2] for m in self.meta)
+
+    def xs(self, sset):
+        return [self.x_dev[sset][int(self.x_off[i]): int(self.x_off[i + 1])] for i in range(len(self.meta))]
+
+    def ys(self):
+        return [self.y_dev[int(self.y_off[i]): int(self.y_off[i + 1])] for i in range(len(self.meta))]
+
+    def ks(self, kc, idx=None):
+        idx = range(len(self.meta)) if idx is None else idx
+        return [k_of(kc, self.meta[i][2]) for i in idx]
+
+
+def time_graphs(torch, dist, launches, K, W, stream, world):
+    """W warm-up replays then EXACTLY K timed replays (round-robin over `launches`),
+    barrier + synchronize on both sides, CUDA events on the launching stream, max over ranks."""
+    for i in range(W):
+        launches[i % len(launches)]()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(K):
+        launches[i % len(launches)]()
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    return ms
+
+
+def cpu_oracle_block(model, bits, kc, seed_tag="cpu"):
+    """Time the oracle (as it stands) on one decoder block's layers (a bounded sample)."""
+    import oracle
+    from synth import gen_perf_layer
+
+    shapes = model_layers(model, fused=False) if model == "llama3_8b" else model_layers(model, fused=True)
+    data = []
+    for name, d_in, d_out in shapes:
+        L = gen_perf_layer(d_in, d_out, bits, seed=layer_seed(seed_tag, name))
+        x = gen_activations(d_in, 1, seed=layer_seed(seed_tag, name, "x"), kind="d" if name in ("down", "d") else "qkv")[0]
+        data.append((name, d_in, L, x))
+    times = {}
+    for name, d_in, L, x in data:
+        t0 = time.perf_counter()
+        oracle.decdec_linear_ref(L["q"], L["s"], L["z"], x, k_of(kc, d_in), rc=L["rc"], rS=L["rS"])
+        times[name] = time.perf_counter() - t0
+    return times
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+# ------------------------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    """The float64 CPU oracle, as it stands, on the host cores (tier: the oracle IS the reference)."""
+    if rank != 0:
+        return
+    import oracle
+    from synth import gen_perf_layer
+
+    model, bits, kc = args.model, args.bits, args.kchunk
+    shapes = model_layers(model, fused=False) if model == "llama3_8b" else model_layers(model, fused=True)
+    data = []
+    for name, d_in, d_out in shapes:
+        L = gen_perf_layer(d_in, d_out, bits, seed=layer_seed("ref", name))
+        X = gen_activations(d_in, 2, seed=layer_seed("ref", name, "x"), kind="d" if name in ("down", "d") else "qkv")
+        data.append((name, d_in, d_out, L, X))
+    per = {n: [] for n, *_ in data}
+
+    def step(i):
+        name, d_in, d_out, L, X = data[i % len(data)]
+        t0 = time.perf_counter()
+        oracle.decdec_linear_ref(L["q"], L["s"], L["z"], X[i % 2], k_of(kc, d_in), rc=L["rc"], rS=L["rS"])
+        return name, time.perf_counter() - t0
+
+    for i in range(args.warmup):
+        step(i)
+    t_all = time.perf_counter()
+    for i in range(args.steps):
+        n, t = step(i)
+        per[n].append(t)
+    t_all = time.perf_counter() - t_all
+    # layer time per shape (extrapolate unmeasured shapes by weight bytes)
+    meas = {n: float(np.mean(v)) for n, v in per.items() if v}
+    bpl = {n: d_in * d_out for n, d_in, d_out, _, _ in data}
+    rate = np.mean([meas[n] / bpl[n] for n in meas])
+    block = sum(meas.get(n, rate * bpl[n]) for n in bpl)
+    tok_s = 1.0 / (MODEL_BLOCKS[model] * block)
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{model} decode linear stack, w{bits} g128 + r4 residual, k_chunk={kc} "
+                               "(each step = one layer call of one block, shapes cycled)", "k_chunk": kc},
+        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} single-layer oracle calls cycling the block's shapes; "
+                                   f"tokens/s = 1/({MODEL_BLOCKS[model]} x sum_shape mean layer time)"},
+        "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "per_layer_s": meas,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------ main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="decdec", choices=["decdec", "reference"])
+    ap.add_argument("--model", default="llama3_8b")
+    ap.add_argument("--bits", type=int, default=3)
+    ap.add_argument("--kchunk", type=int, default=21, help="headline k_chunk (21 = 2.05%% of channels)")
+    ap.add_argument("--sweep", default="0,4,8,16,21,32", help="k_chunk sweep (µs/layer per shape + tokens/s)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nx", type=int, default=4, help="distinct activation sets cycled across steps")
+    ap.add_argument("--quick", action="store_true", help="headline step only (for ncu launch lists)")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_20185_b200 as dd
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = "cuda"
+    stream = torch.cuda.current_stream()
+    hbm_peak, hbm_src, pcie_peak, pcie_src = load_peaks()
+
+    t_build = time.time()
+    M = Model(dd, torch, args.model, args.bits, rank, world, args.nx, dev)
+    sweep = sorted({int(v) for v in args.sweep.split(",") if v != ""} | {args.kchunk})
+    if args.quick:
+        sweep, args.no_cpu_baseline = [args.kchunk], True
+    max_k = k_of(max(sweep), M.max_d_in)
+    ws = dd.Workspace(max_k, M.max_d_out)
+    torch.cuda.synchronize()
+    t_build = time.time() - t_build
+    n_layers = len(M.meta)
+
+    # ---- full decode-step graphs per k_chunk -------------------------------------------------
+    def step_launchers(kc):
+        if world == 1:
+            stacks = [dd.Stack(M.layers, M.ks(kc), M.xs(s), M.ys(), ws) for s in range(args.nx)]
+            return stacks, [st.launch for st in stacks], stacks[0].kernels
+        # TP: per-layer decdec_linear on the shard + NCCL all-gather, captured by torch.cuda.graph
+        full = [torch.empty(m[3] * world, dtype=torch.float16, device=dev) for m in M.meta]
+        graphs = []
+        for s in range(args.nx):
+            xs, ys = M.xs(s), M.ys()
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for i, lin in enumerate(M.layers):   # warm NCCL outside capture
+                    lin(xs[i], M.ks(kc, [i])[0], y=ys[i], workspace=ws)
+                    dist.all_gather_into_tensor(full[i], ys[i])
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                for i, lin in enumerate(M.layers):
+                    lin(xs[i], M.ks(kc, [i])[0], y=ys[i], workspace=ws)
+                    dist.all_gather_into_tensor(full[i], ys[i])
+            graphs.append(g)
+        kern = sum(2 if k else 1 for k in M.ks(kc))
+        return graphs, [g.replay for g in graphs], kern
+
+    results = {}
+    headline = None
+    clocks = None
+    for kc in sweep:
+        objs, launches, kernels = step_launchers(kc)
+        is_head = kc == args.kchunk
+        sampler = ClockSampler(local) if (is_head and rank == 0) else None
+        ms = time_graphs(torch, dist, launches, args.steps, max(args.warmup, 3), stream, world)
+        if sampler is not None:
+            clocks = sampler.stop()
+        results[kc] = {"ms_per_step": ms, "tokens_per_s": 1e3 / ms, "kernels_per_step": kernels}
+        if is_head:
+            headline = (ms, kernels)
+        del objs
+
+    # ---- per-shape µs per layer (graph of the n_blocks instances of one shape) --------------
+    shape_names = []
+    for (_, name, _, _) in M.meta:
+        if name not in shape_names:
+            shape_names.append(name)
+    per_shape = {}
+    if world == 1 and not args.quick:
+        for name in shape_names:
+            idx = [i for i, m in enumerate(M.meta) if m[1] == name]
+            d_in, d_out = M.meta[idx[0]][2], M.meta[idx[0]][3]
+            per_shape[name] = {"d_in": d_in, "d_out": d_out}
+            for kc in sweep:
+                lay = [M.layers[i] for i in idx]
+                xs = [M.xs(s) for s in range(args.nx)]
+                stacks = [dd.Stack(lay, M.ks(kc, idx), [xs[s][i] for i in idx], [M.ys()[i] for i in idx], ws)
+                          for s in range(args.nx)]
+                ms = time_graphs(torch, dist, [st.launch for st in stacks], max(8, args.steps // 4), 3, stream, 1)
+                us = 1e3 * ms / len(idx)
+                k = k_of(kc, d_in)
+                bh, bp = bytes_hbm(d_in, d_out, args.bits), bytes_pcie(k, d_out)
+                t_roof = max(bh / (hbm_peak * 1e3), bp / (pcie_peak * 1e3))  # µs
+                per_shape[name][str(kc)] = {"us": round(us, 3), "k": k, "hbm_GBps": round(bh / us / 1e3, 1),
+                                            "pcie_GBps": round(bp / us / 1e3, 2), "roofline_us": round(t_roof, 3),
+                                            "roofline_frac": round(t_roof / us, 3)}
+                for st in stacks:
+                    st.close()
+
+    # ---- e2e through the public API: H2D inputs + step + D2H outputs ------------------------
+    e2e = None
+    if world == 1 and not args.quick:
+        x_pinned = [torch.from_numpy(h).pin_memory() for h in M.x_host]
+        y_pinned = torch.empty(M.y_dev.numel(), dtype=torch.float16).pin_memory()
+        stack = dd.Stack(M.layers, M.ks(args.kchunk), M.xs(0), M.ys(), ws)
+
+        def e2e_step_factory(i):
+            def f():
+                M.x_dev[0].copy_(x_pinned[i % len(x_pinned)], non_blocking=True)
+                stack.launch()
+                y_pinned.copy_(M.y_dev, non_blocking=True)
+            return f
+        ms_e2e = time_graphs(torch, dist, [e2e_step_factory(i) for i in range(args.nx)], args.steps,
+                             max(args.warmup, 3), stream, world)
+        e2e = {"value": 1e3 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(M.x_dev[0].numel() * 2),
+               "d2h_bytes_per_step": int(M.y_dev.numel() * 2), "ms_per_step": ms_e2e,
+               "api": "paper_2412_20185_b200.Stack (decdec_stack_launch) + pinned H2D/D2H copies"}
+        stack.close()
+
+    # ---- roofline of the dominant kernel ------------------------------------------------------
+    ms_head, kernels_head = headline
+    step_hbm = sum(bytes_hbm(m[2], m[3], args.bits) for m in M.meta)
+    step_pcie = sum(bytes_pcie(k_of(args.kchunk, m[2]), m[3]) for m in M.meta)
+    t_roof_step = sum(max(bytes_hbm(m[2], m[3], args.bits) / (hbm_peak * 1e6),
+                          bytes_pcie(k_of(args.kchunk, m[2]), m[3]) / (pcie_peak * 1e6)) for m in M.meta)  # ms
+    roofline = None
+    if per_shape:
+        dom = max(per_shape, key=lambda n: per_shape[n][str(args.kchunk)]["us"] *
+                  sum(1 for m in M.meta if m[1] == n))
+        e = per_shape[dom][str(args.kchunk)]
+        d_in, d_out = per_shape[dom]["d_in"], per_shape[dom]["d_out"]
+        bh, bp = bytes_hbm(d_in, d_out, args.bits), bytes_pcie(e["k"], d_out)
+        pcie_bound = bp / pcie_peak > bh / hbm_peak
+        ach = (bp if pcie_bound else bh) / e["us"] / 1e3
+        peak = pcie_peak if pcie_bound else hbm_peak
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+                traffic = json.load(f).get(f"{dom}/{args.kchunk}")
+        except Exception:
+            pass
+        roofline = {
+            "bound": "pcie" if pcie_bound else "hbm", "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
+            "frac": round(ach / peak, 4), "traffic": traffic,
+            "kernel": f"select + k_linear<{args.bits},4> on {dom} ({d_in}x{d_out}), k={e['k']}",
+            "algorithmic_bytes": {"hbm": bh, "pcie": bp},
+            "hbm_frac": round(bh / e["us"] / 1e3 / hbm_peak, 4), "pcie_frac": round(bp / e["us"] / 1e3 / pcie_peak, 4),
+            "layer_roofline_frac": e["roofline_frac"],
+            "peak_source": {"hbm": hbm_src, "pcie": pcie_src},
+            "step_roofline_ms": round(t_roof_step, 4), "step_roofline_frac": round(t_roof_step / ms_head, 4),
+        }
+
+    # ---- CPU baseline (oracle on host cores, rank 0, N = 1) ----------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        times = cpu_oracle_block(args.model, args.bits, args.kchunk)
+        blk = sum(times.values())
+        cpu = {"value": 1.0 / (M.n_blocks * blk), "unit": "tokens/s", "cores": blas_threads(), "kind": "oracle",
+               "sample": f"one decoder block ({', '.join(times)}) through oracle.decdec_linear_ref at "
+                         f"k_chunk={args.kchunk}, x {M.n_blocks} blocks; {blk:.1f} s of CPU work",
+               "per_layer_s": {k: round(v, 3) for k, v in times.items()}}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(1e3 / ms_head, 2), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_head, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": f"int{args.bits} weights x f16 activations -> f32 accumulate (f16 out); int4 residual",
+            "data": "synthetic (seeded; random packed codes, outlier-heavy Student-t activations)",
+            "config": {"workload": f"{args.model} decode linear stack: {n_layers // M.n_blocks} layers x "
+                                   f"{M.n_blocks} blocks, w{args.bits} g128, r4 residual in pinned host memory, "
+                                   f"exact Top-k, k_chunk={args.kchunk}",
+                       "k_chunk": args.kchunk, "layers_per_step": n_layers,
+                       "parallelism": f"tp{world} (output-feature shards + NCCL all-gather)" if world > 1 else "single GPU",
+                       "l2": f"inputs larger than L2: {step_hbm / 1e9:.2f} GB weights streamed per step",
+                       "x_sets": args.nx},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": kernels_head * args.steps,
+            "clocks": clocks,
+            "sweep": {str(k): {"tokens_per_s": round(v["tokens_per_s"], 2), "ms_per_step": round(v["ms_per_step"], 4),
+                               "slowdown_vs_k0": round(v["ms_per_step"] / results[0]["ms_per_step"], 4)
+                               if 0 in results else None}
+                      for k, v in results.items()},
+            "per_layer_us": per_shape,
+            "step_bytes": {"hbm": step_hbm, "pcie": step_pcie},
+            "build_s": round(t_build, 1),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

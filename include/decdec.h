@@ -123,6 +123,21 @@ decdec_status decdec_select(const uint16_t* x, int32_t d_in, int32_t k, int32_t 
 /* Number of channels selected for (d_in, k, chunk); -1 on invalid arguments. */
 int32_t decdec_num_selected(int32_t d_in, int32_t k, int32_t chunk);
 
+/* ------------------------------------------------------------------ native step executor */
+/* A decode step's sequence of layer calls captured once into a CUDA graph (one stream,
+ * layer i+1 after layer i; inside a layer the selector and the fused kernel overlap via
+ * programmatic dependent launch).  Buffers x[i], y[i] and the shared workspace are
+ * bound at creation; replays read whatever those buffers hold.  All layers are validated
+ * before capture; on error nothing is created.  chunk applies to every layer; k[i] is the
+ * per-layer k (or k_chunk when chunk > 0). */
+typedef struct decdec_stack decdec_stack;
+decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
+                                  const uint16_t* const* x, uint16_t* const* y, void* ws, size_t ws_bytes,
+                                  decdec_stream_t stream, decdec_stack** out);
+decdec_status decdec_stack_launch(decdec_stack* s, decdec_stream_t stream);
+int32_t decdec_stack_kernels(const decdec_stack* s); /* kernels per launch, -1 if NULL */
+void decdec_stack_destroy(decdec_stack* s);
+
 /* ------------------------------------------------------------------ offline, host-only */
 /* Pack base codes q (u8 [d_in][d_out], logical W layout, values < 2^bits) into W3K/W4K
  * (uint32 [d_out][d_in*bits/32]).  out_bytes must be >= d_out*d_in*bits/8. */

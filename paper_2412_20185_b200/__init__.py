@@ -22,9 +22,13 @@ from ._lib import (  # noqa: F401
     decdec_pack_weights,
     decdec_plan_string,
     decdec_select,
+    decdec_stack_create,
+    decdec_stack_destroy,
+    decdec_stack_kernels,
+    decdec_stack_launch,
     decdec_status_string,
     decdec_version,
     decdec_workspace_bytes,
     decdec_workspace_init,
 )
-from .layer import HostBuffer, QuantLinear, Workspace, pack_residual_into, pack_weights, select  # noqa: F401
+from .layer import HostBuffer, QuantLinear, Stack, Workspace, pack_residual_into, pack_weights, select  # noqa: F401

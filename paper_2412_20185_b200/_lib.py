@@ -53,6 +53,10 @@ def _load():
         "decdec_debug_unpack_weights": (I32, [Lp, VP, VP]),
         "decdec_plan_string": (I32, [Lp, I32, ctypes.c_char_p, SZ]),
         "decdec_launches_per_call": (I32, [I32]),
+        "decdec_stack_create": (I32, [Lp, I32, P(I32), I32, P(VP), P(VP), VP, SZ, VP, P(VP)]),
+        "decdec_stack_launch": (I32, [VP, VP]),
+        "decdec_stack_kernels": (I32, [VP]),
+        "decdec_stack_destroy": (None, [VP]),
         "decdec_status_string": (ctypes.c_char_p, [I32]),
         "decdec_version": (ctypes.c_char_p, []),
     }
@@ -68,7 +72,8 @@ EXPORTED = [
     "decdec_workspace_bytes", "decdec_workspace_init", "decdec_linear", "decdec_gemv", "decdec_select",
     "decdec_num_selected", "decdec_pack_weights", "decdec_pack_residual", "decdec_host_alloc",
     "decdec_host_free", "decdec_debug_unpack_weights", "decdec_plan_string", "decdec_launches_per_call",
-    "decdec_status_string", "decdec_version",
+    "decdec_status_string", "decdec_version", "decdec_stack_create", "decdec_stack_launch",
+    "decdec_stack_kernels", "decdec_stack_destroy",
 ]
 
 
@@ -145,3 +150,27 @@ def decdec_status_string(s: int) -> str:
 
 def decdec_version() -> str:
     return _lib.decdec_version().decode()
+
+
+def decdec_stack_create(layers, ks, chunk, xs, ys, ws, ws_bytes, stream=0) -> int:
+    n = len(layers)
+    arr = (decdec_layer * n)(*layers)
+    karr = (ctypes.c_int32 * n)(*[int(k) for k in ks])
+    xarr = (ctypes.c_void_p * n)(*[int(p) for p in xs])
+    yarr = (ctypes.c_void_p * n)(*[int(p) for p in ys])
+    out = ctypes.c_void_p()
+    _check(_lib.decdec_stack_create(arr, n, karr, chunk, xarr, yarr, _vp(ws), ws_bytes, _vp(stream), ctypes.byref(out)),
+           "decdec_stack_create")
+    return int(out.value)
+
+
+def decdec_stack_launch(s, stream=0):
+    _check(_lib.decdec_stack_launch(_vp(s), _vp(stream)), "decdec_stack_launch")
+
+
+def decdec_stack_kernels(s) -> int:
+    return int(_lib.decdec_stack_kernels(_vp(s)))
+
+
+def decdec_stack_destroy(s):
+    _lib.decdec_stack_destroy(_vp(s))

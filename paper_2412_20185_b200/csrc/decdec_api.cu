@@ -259,8 +259,22 @@ decdec_status decdec_gemv(const decdec_layer* L, const uint16_t* x, uint16_t* y,
   return launch_linear(p, pl, L->w_bits, 4, false, (cudaStream_t)stream);
 }
 
-decdec_status decdec_linear(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk, uint16_t* y,
-                            int32_t* sel, void* ws, size_t ws_bytes, decdec_stream_t stream) {
+}  // extern "C"
+
+namespace {
+
+// Validated, planned launch of one layer (no CUDA API calls except the launches), so it
+// can run inside stream capture.
+struct Prepared {
+  LinearParams p;
+  Plan pl;
+  int k, chunk, bits, rbits;
+  const uint16_t* x;
+  int32_t* sel;
+};
+
+decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk, uint16_t* y,
+                             int32_t* sel, void* ws, size_t ws_bytes, Prepared* out) {
   decdec_status s = check_layer(L, k > 0);
   if (s != DECDEC_OK) return s;
   if (!x || !y) return DECDEC_EINVAL;
@@ -268,35 +282,122 @@ decdec_status decdec_linear(const decdec_layer* L, const uint16_t* x, int32_t k,
   const int k_sel = n_selected(L->d_in, k, chunk);
   if (k_sel < 0) return DECDEC_EINVAL;
   if ((s = ensure_attrs()) != DECDEC_OK) return s;
-  Plan pl;
-  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &pl)) != DECDEC_OK) return s;
-  LinearParams p = base_params(L, x, y, pl);
-  cudaStream_t st = (cudaStream_t)stream;
-  if (k_sel == 0) return launch_linear(p, pl, L->w_bits, 4, false, st);
+  Prepared P{};
+  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &P.pl)) != DECDEC_OK) return s;
+  P.p = base_params(L, x, y, P.pl);
+  P.k = k;
+  P.chunk = chunk;
+  P.bits = L->w_bits;
+  P.rbits = L->r_bits;
+  P.x = x;
+  P.sel = sel;
+  if (k_sel > 0) {
+    if (!ws) return DECDEC_EINVAL;
+    const WsLayout wl = ws_layout(k_sel, L->d_out);
+    if (wl.total > ws_bytes) return DECDEC_ESPACE;
+    if (!aligned16(ws)) return DECDEC_EALIGN;
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    LinearParams& p = P.p;
+    p.k_sel = k_sel;
+    p.idx = reinterpret_cast<const int*>(base + wl.idx);
+    p.xs = reinterpret_cast<const uint16_t*>(base + wl.xs);
+    p.r_rows = static_cast<const uint8_t*>(L->r_rows);
+    p.r_scales = L->r_scales;
+    p.r_row_bytes = L->d_out * L->r_bits / 8;
+    p.ob = reinterpret_cast<float*>(base + wl.ob);
+    p.part = reinterpret_cast<float*>(base + wl.part);
+    p.sdev = reinterpret_cast<uint16_t*>(base + wl.sdev);
+    p.cnt = reinterpret_cast<uint32_t*>(base + wl.cnt);
+    p.n_seg = (L->d_out + kSegCols - 1) / kSegCols;
+    if (p.n_seg > kCntSlots) return DECDEC_EUNSUPPORTED;
+    p.n_rb = (k_sel + kRB - 1) / kRB;
+    p.n_items = p.n_seg * p.n_rb;
+  }
+  *out = P;
+  return DECDEC_OK;
+}
 
-  if (!ws) return DECDEC_EINVAL;
-  const WsLayout wl = ws_layout(k_sel, L->d_out);
-  if (wl.total > ws_bytes) return DECDEC_ESPACE;
-  if (!aligned16(ws)) return DECDEC_EALIGN;
-  uint8_t* base = static_cast<uint8_t*>(ws);
-  p.k_sel = k_sel;
-  p.idx = reinterpret_cast<const int*>(base + wl.idx);
-  p.xs = reinterpret_cast<const uint16_t*>(base + wl.xs);
-  p.r_rows = static_cast<const uint8_t*>(L->r_rows);
-  p.r_scales = L->r_scales;
-  p.r_row_bytes = L->d_out * L->r_bits / 8;
-  p.ob = reinterpret_cast<float*>(base + wl.ob);
-  p.part = reinterpret_cast<float*>(base + wl.part);
-  p.sdev = reinterpret_cast<uint16_t*>(base + wl.sdev);
-  p.cnt = reinterpret_cast<uint32_t*>(base + wl.cnt);
-  p.n_seg = (L->d_out + kSegCols - 1) / kSegCols;
-  if (p.n_seg > kCntSlots) return DECDEC_EUNSUPPORTED;
-  p.n_rb = (k_sel + kRB - 1) / kRB;
-  p.n_items = p.n_seg * p.n_rb;
-  if ((s = launch_select(x, L->d_in, k, chunk, reinterpret_cast<int*>(base + wl.idx),
-                         reinterpret_cast<uint16_t*>(base + wl.xs), sel, st)) != DECDEC_OK)
+decdec_status enqueue_linear(const Prepared& P, cudaStream_t st) {
+  if (P.p.k_sel == 0) return launch_linear(P.p, P.pl, P.bits, 4, false, st);
+  decdec_status s = launch_select(P.x, P.p.d_in, P.k, P.chunk, const_cast<int*>(P.p.idx),
+                                  const_cast<uint16_t*>(P.p.xs), P.sel, st);
+  if (s != DECDEC_OK) return s;
+  return launch_linear(P.p, P.pl, P.bits, P.rbits, true, st);
+}
+
+}  // namespace
+
+struct decdec_stack {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int n_layers = 0, n_kernels = 0;
+};
+
+extern "C" {
+
+decdec_status decdec_linear(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk, uint16_t* y,
+                            int32_t* sel, void* ws, size_t ws_bytes, decdec_stream_t stream) {
+  Prepared P;
+  decdec_status s = prepare_linear(L, x, k, chunk, y, sel, ws, ws_bytes, &P);
+  if (s != DECDEC_OK) return s;
+  return enqueue_linear(P, (cudaStream_t)stream);
+}
+
+decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
+                                  const uint16_t* const* x, uint16_t* const* y, void* ws, size_t ws_bytes,
+                                  decdec_stream_t stream, decdec_stack** out) {
+  if (!layers || n_layers <= 0 || !k || !x || !y || !out) return DECDEC_EINVAL;
+  *out = nullptr;
+  Prepared* P = new Prepared[n_layers];
+  decdec_status s = DECDEC_OK;
+  int n_kernels = 0;
+  for (int i = 0; i < n_layers && s == DECDEC_OK; ++i) {
+    s = prepare_linear(&layers[i], x[i], k[i], chunk, y[i], nullptr, ws, ws_bytes, &P[i]);
+    n_kernels += P[i].p.k_sel > 0 ? 2 : 1;
+  }
+  if (s != DECDEC_OK) {
+    delete[] P;
     return s;
-  return launch_linear(p, pl, L->w_bits, L->r_bits, true, st);
+  }
+  (void)stream;  // capture runs on a private stream (the legacy NULL stream cannot capture)
+  cudaStream_t st = nullptr;
+  cudaError_t e0 = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e0 != cudaSuccess) {
+    delete[] P;
+    return cuda_status(e0);
+  }
+  decdec_stack* g = new decdec_stack();
+  cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  for (int i = 0; i < n_layers && e == cudaSuccess && s == DECDEC_OK; ++i) s = enqueue_linear(P[i], st);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+  cudaStreamDestroy(st);
+  delete[] P;
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess && s == DECDEC_OK) e = cudaGraphInstantiate(&g->exec, graph, 0);
+  g->graph = graph;
+  g->n_layers = n_layers;
+  g->n_kernels = n_kernels;
+  if (e != cudaSuccess || s != DECDEC_OK) {
+    decdec_stack_destroy(g);
+    return s != DECDEC_OK ? s : cuda_status(e);
+  }
+  *out = g;
+  return DECDEC_OK;
+}
+
+decdec_status decdec_stack_launch(decdec_stack* g, decdec_stream_t stream) {
+  if (!g || !g->exec) return DECDEC_EINVAL;
+  return cuda_status(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+}
+
+int32_t decdec_stack_kernels(const decdec_stack* g) { return g ? g->n_kernels : -1; }
+
+void decdec_stack_destroy(decdec_stack* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
 }
 
 decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out, decdec_stream_t stream) {

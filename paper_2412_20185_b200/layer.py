@@ -165,3 +165,29 @@ def select(x: torch.Tensor, k: int, chunk: int = 0, stream=None):
     xs = torch.empty(max(n, 1), dtype=torch.float16, device=x.device)
     _lib.decdec_select(x.data_ptr(), x.numel(), k, chunk, idx.data_ptr(), xs.data_ptr(), _stream_ptr(stream))
     return idx[:n], xs[:n]
+
+
+class Stack:
+    """A decode step's layer calls as one native CUDA graph (decdec_stack_*)."""
+
+    def __init__(self, layers, ks, xs, ys, workspace, chunk: int = 0, stream=None):
+        self.layers = list(layers)
+        self._keep = (list(xs), list(ys), workspace)
+        self.handle = _lib.decdec_stack_create([l.struct for l in self.layers], ks, chunk,
+                                               [x.data_ptr() for x in xs], [y.data_ptr() for y in ys],
+                                               workspace.ptr, workspace.nbytes, _stream_ptr(stream))
+        self.kernels = _lib.decdec_stack_kernels(self.handle)
+
+    def launch(self, stream=None):
+        _lib.decdec_stack_launch(self.handle, _stream_ptr(stream))
+
+    def close(self):
+        if self.handle:
+            _lib.decdec_stack_destroy(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -5,11 +5,13 @@ distributions of the paper's workloads (SURVEY.md §8(
 """
 
 from .inputs import (  # noqa: F401
+    MODEL_BLOCKS,
     SHAPES,
     layer_seed,
     gen_weight_fp16,
     gen_activations,
     gen_special_activations,
     gen_perf_layer,
+    gen_perf_layer_device,
     model_layers,
 )

@@ -101,3 +101,26 @@ def gen_perf_layer(d_in: int, d_out: int, bits: int, seed: int, group: int = 128
         out["rc"] = rng.integers(-7, 8, size=(d_in, d_out), dtype=np.int8)
         out["rS"] = (np.median(s.astype(np.float64), axis=0) / 14.0).astype(np.float16)
     return out
+
+
+def gen_perf_layer_device(d_in: int, d_out: int, bits: int, seed: int, device="cuda", group: int = 128):
+    """Perf-harness layer drawn directly on the GPU (torch RNG, seeded): uniformly random
+    packed code bits (every layout here is a bijection between code bits and words, so
+    random words == iid uniform codes), scales/zeros per the §8(d) recipe, and random
+    residual row bytes (nibbles uniform on [0, 15]) plus residual scales.
+    Returns device tensors: w uint8 [d_out * d_in * bits / 8], s fp16 [d_out * G],
+    z uint8 [d_out * G], r uint8 [d_in * d_out / 2], rS fp16 [d_out]."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed & 0x7FFFFFFFFFFFFFFF)
+    G = d_in // group
+    nb = d_out * d_in * bits // 8
+    w = torch.randint(0, 256, (nb,), dtype=torch.uint8, device=device, generator=g)
+    zlo = 3 if bits == 3 else 7
+    z = torch.randint(zlo, zlo + 2, (d_out * G,), dtype=torch.uint8, device=device, generator=g)
+    ln = torch.exp(torch.randn(d_out * G, device=device, generator=g) * 0.25)
+    s = (0.02 * 12 ** 0.5 / (1 << bits) * ln).to(torch.float16)
+    r = torch.randint(0, 256, (d_in * d_out // 2,), dtype=torch.uint8, device=device, generator=g)
+    rS = (s.float().view(d_out, G).median(dim=1).values / 14.0).to(torch.float16)
+    return dict(w=w, s=s, z=z, r=r, rS=rS)

@@ -188,3 +188,25 @@ def test_rejects_unmapped_residual():
     assert e.value.status == -3
     with pytest.raises(dd.DecdecError):
         lin(x, 2000, workspace=ws)
+
+
+def test_stack_graph_matches_per_layer_calls():
+    """decdec_stack (one captured CUDA graph) == the same layers called one by one."""
+    shapes = [(4096, 1024), (1024, 4096), (4096, 2048)]
+    lins, xs = [], []
+    for i, (d_in, d_out) in enumerate(shapes):
+        L = gen_perf_layer(d_in, d_out, 3, seed=100 + i)
+        lins.append(dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"]))
+        xs.append(to_dev(gen_activations(d_in, 1, seed=200 + i)[0]))
+    ks = [oracle.k_from_kchunk(21, d_in) for d_in, _ in shapes]
+    ws = dd.Workspace(max(ks), 4096)
+    ref = [lin(x, k, workspace=ws).clone() for lin, x, k in zip(lins, xs, ks)]
+    ys = [torch.empty(d_out, dtype=torch.float16, device=DEV) for _, d_out in shapes]
+    st = dd.Stack(lins, ks, xs, ys, ws)
+    assert st.kernels == 6
+    for _ in range(3):
+        st.launch()
+    torch.cuda.synchronize()
+    for a, b in zip(ys, ref):
+        assert torch.equal(a, b)
+    st.close()
