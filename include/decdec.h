@@ -161,6 +161,12 @@ void decdec_host_free(void* p);
 decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out,
                                           decdec_stream_t stream);
 
+/* Debug timelines: while buf != NULL every launch records %globaltimer (ns) events into buf
+ * (u64: [0] selector start, [1] selector end, then per CTA 9 events: start, first bulk copy
+ * issued, x loaded, first stage landed, GEMV done, selector visible, selection staged, gather
+ * done).  bytes >= (2 + 1024*9)*8.  Not thread-safe; NULL disables (default). */
+decdec_status decdec_debug_trace(void* buf, size_t bytes);
+
 /* Launch plan chosen for a layer (tile rows, consumer warps, stages, grid) as text. */
 decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, size_t buf_bytes);
 

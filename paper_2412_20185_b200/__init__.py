@@ -10,6 +10,7 @@ from ._lib import (  # noqa: F401
     EXPORTED,
     LIB_PATH,
     DecdecError,
+    decdec_debug_trace,
     decdec_debug_unpack_weights,
     decdec_gemv,
     decdec_host_alloc,

@@ -53,6 +53,7 @@ def _load():
         "decdec_debug_unpack_weights": (I32, [Lp, VP, VP]),
         "decdec_plan_string": (I32, [Lp, I32, ctypes.c_char_p, SZ]),
         "decdec_launches_per_call": (I32, [I32]),
+        "decdec_debug_trace": (I32, [VP, SZ]),
         "decdec_stack_create": (I32, [Lp, I32, P(I32), I32, P(VP), P(VP), VP, SZ, VP, P(VP)]),
         "decdec_stack_launch": (I32, [VP, VP]),
         "decdec_stack_kernels": (I32, [VP]),
@@ -73,7 +74,7 @@ EXPORTED = [
     "decdec_num_selected", "decdec_pack_weights", "decdec_pack_residual", "decdec_host_alloc",
     "decdec_host_free", "decdec_debug_unpack_weights", "decdec_plan_string", "decdec_launches_per_call",
     "decdec_status_string", "decdec_version", "decdec_stack_create", "decdec_stack_launch",
-    "decdec_stack_kernels", "decdec_stack_destroy",
+    "decdec_stack_kernels", "decdec_stack_destroy", "decdec_debug_trace",
 ]
 
 
@@ -174,3 +175,7 @@ def decdec_stack_kernels(s) -> int:
 
 def decdec_stack_destroy(s):
     _lib.decdec_stack_destroy(_vp(s))
+
+
+def decdec_debug_trace(buf, nbytes):
+    _check(_lib.decdec_debug_trace(_vp(buf), nbytes), "decdec_debug_trace")

@@ -2,6 +2,7 @@
 // launches of the sm_100a kernels in select.cuh / linear.cuh.
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -28,46 +29,78 @@ int device_sms() {
   return cache[dev];
 }
 
+unsigned long long* g_trace = nullptr;  // debug timelines (decdec_debug_trace)
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int gcd(int a, int b) { while (b) { int t = a % b; a = b; b = t; } return a; }
 
 struct Plan {
-  int G, RP, RPT, TR, NC, stages, n_tiles, grid, NGW;
-  uint32_t stage_bytes, off_s, off_z;
+  int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, NGW;
+  uint32_t stage_bytes, off_s, off_z, off_sel;
   size_t smem;
 };
 
 constexpr size_t kSmemBudget = 200 * 1024;
 
+// Launch plan: enumerate (consumer warps NC, rows per slot RPS); pick the one minimising the
+// busiest CTA's bytes (ceil(tiles / SMs) x (stage bytes + a per-tile overhead equivalent)),
+// ties -> more consumer warps.  DECDEC_PLAN="NC,RPS" overrides (tuning).
 decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl) {
-  Plan p{};
-  p.G = d_in / DECDEC_GROUP;
+  const int G = d_in / DECDEC_GROUP;
   const int sms = device_sms();
-  p.RP = 1;
-  while (p.RP * 2 * p.G <= 384) p.RP *= 2;  // <= 12 consumer warps
-  while (p.RP > 1 && (d_out / p.RP < sms || d_out % p.RP)) p.RP /= 2;
-  const int unit = 16 / gcd(p.G, 16);  // TR * G % 16 == 0 for the zeros bulk copy
-  p.RPT = 1;
-  while ((p.RP * p.RPT) % unit) p.RPT *= 2;
-  p.TR = p.RP * p.RPT;
-  if (d_out % p.TR || kSegCols % p.TR) return DECDEC_EUNSUPPORTED;
-  p.NC = (p.RP * p.G + 31) / 32;
-  if (p.NC > 12) return DECDEC_EUNSUPPORTED;
+  const bool small_g = G <= 32 && 32 % G == 0;
+  const int nkw = small_g ? 0 : (G + 31) / 32;
   const uint32_t row_bytes = (uint32_t)d_in * bits / 8;
-  p.off_s = (uint32_t)p.TR * row_bytes;
-  p.off_z = p.off_s + (uint32_t)p.TR * p.G * 2;
-  p.stage_bytes = (uint32_t)align_up(p.off_z + (uint32_t)p.TR * p.G, 16);
-  const size_t red = (size_t)2 * p.TR * p.G * 4;
-  const size_t avail = kSmemBudget - red - 16 * 8;
-  p.stages = (int)(avail / p.stage_bytes);
-  if (p.stages > 8) p.stages = 8;
-  if (p.stages < 2) return DECDEC_EUNSUPPORTED;
-  p.n_tiles = d_out / p.TR;
-  p.grid = p.n_tiles < sms ? p.n_tiles : sms;
-  p.NGW = k_sel > 0 ? 2 : 0;
-  p.smem = (size_t)p.stages * p.stage_bytes + red + (size_t)2 * p.stages * 8;
-  *pl = p;
+  static int env_nc = -1, env_rps = -1;
+  if (env_nc < 0) {
+    const char* e = getenv("DECDEC_PLAN");
+    env_nc = 0;
+    env_rps = 0;
+    if (e) sscanf(e, "%d,%d", &env_nc, &env_rps);
+  }
+  Plan best{};
+  double best_cost = 1e300;
+  bool have = false;
+  for (int nc = 1; nc <= 12; ++nc) {
+    if (small_g ? (nc & (nc - 1)) != 0 : (nc % nkw || ((nc / nkw) & (nc / nkw - 1)) != 0)) continue;
+    for (int rps = 1; rps <= kMaxRPS; rps *= 2) {
+      if (env_nc > 0 && (nc != env_nc || rps != env_rps)) continue;
+      Plan p{};
+      p.G = G;
+      p.NKW = nkw;
+      p.NC = nc;
+      p.NSLOTS = small_g ? nc * (32 / G) : nc / nkw;
+      p.RPS = rps;
+      p.TR = p.NSLOTS * rps;
+      if (p.TR > kSegCols || kSegCols % p.TR || d_out % p.TR || (p.TR * G) % 16) continue;
+      p.off_s = (uint32_t)p.TR * row_bytes;
+      p.off_z = p.off_s + (uint32_t)p.TR * G * 2;
+      p.stage_bytes = (uint32_t)align_up(p.off_z + (uint32_t)p.TR * G, 16);
+      const size_t red = (size_t)2 * p.NSLOTS * 4 * (nkw ? nkw : 1) * 4;
+      const size_t sel = align_up((size_t)k_sel * 6, 16);
+      const size_t avail = kSmemBudget - red - 16 * 8 - sel;
+      p.stages = (int)(avail / p.stage_bytes);
+      if (p.stages > 8) p.stages = 8;
+      if (p.stages < 2) continue;
+      p.n_tiles = d_out / p.TR;
+      // k > 0: leave one SM free for the selector kernel that runs concurrently (PDL)
+      const int max_grid = k_sel > 0 ? sms - 1 : sms;
+      p.grid = p.n_tiles < max_grid ? p.n_tiles : max_grid;
+      p.NGW = k_sel > 0 ? 2 : 0;
+      p.off_sel = (uint32_t)((size_t)p.stages * p.stage_bytes + red + (size_t)2 * p.stages * 8);
+      p.smem = p.off_sel + sel;
+      const double waves = (double)((p.n_tiles + sms - 1) / sms);
+      const double cost = waves * ((double)p.stage_bytes + 3072.0) * (nc < 4 ? 1.0 + 0.15 * (4 - nc) : 1.0);
+      if (!have || cost < best_cost * 0.999 || (cost <= best_cost * 1.001 && p.NC > best.NC)) {
+        best = p;
+        best_cost = cost;
+        have = true;
+      }
+    }
+  }
+  if (!have) return DECDEC_EUNSUPPORTED;
+  *pl = best;
   return DECDEC_OK;
 }
 
@@ -103,12 +136,13 @@ decdec_status g_attr_status = DECDEC_OK;
 void init_attrs() {
   decdec_status s = DECDEC_OK;
   const size_t lin = 227 * 1024;
+  if (s == DECDEC_OK) s = set_smem_attr(k_select<1>, 160 * 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_select<2>, 160 * 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_select<4>, 160 * 1024);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 16>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 16>, lin);
-  if (s == DECDEC_OK) s = set_smem_attr(k_select<1024>, 64 * 1024);
-  if (s == DECDEC_OK) s = set_smem_attr(k_select<256>, 64 * 1024);
   g_attr_status = s;
 }
 decdec_status ensure_attrs() {
@@ -154,22 +188,21 @@ decdec_status check_layer(const decdec_layer* L, bool need_residual) {
 int n_selected(int d_in, int k, int chunk) {
   if (k < 0 || d_in <= 0) return -1;
   if (chunk == 0) return k <= d_in ? k : -1;
-  if (chunk < 32 || chunk > 32768 || k > chunk) return -1;
+  if (chunk < 32 || chunk > 32768 || chunk % 8 || k > chunk) return -1;
   const int full = d_in / chunk, rem = d_in % chunk;
   return full * k + (rem < k ? rem : k);
 }
 
 decdec_status launch_select(const uint16_t* x, int d_in, int k, int chunk, int* idx, uint16_t* xs, int* sel,
                             cudaStream_t st) {
-  if (chunk == 0) {
-    k_select<1024><<<1, 1024, (size_t)d_in * 2, st>>>(x, d_in, k, 0, idx, xs, sel);
-  } else {
-    const int nseg = (d_in + chunk - 1) / chunk;
-    if (chunk <= 4096)
-      k_select<256><<<nseg, 256, (size_t)chunk * 2, st>>>(x, d_in, k, chunk, idx, xs, sel);
-    else
-      k_select<1024><<<nseg, 1024, (size_t)chunk * 2, st>>>(x, d_in, k, chunk, idx, xs, sel);
-  }
+  const int n = chunk ? (chunk < d_in ? chunk : d_in) : d_in;
+  int nt = 32, C = 1;
+  select_geometry(n, &nt, &C);
+  const int nseg = chunk ? (d_in + chunk - 1) / chunk : 1;
+  const size_t sm = select_smem_bytes(nt, n);
+  if (C == 1) k_select<1><<<nseg, nt, sm, st>>>(x, d_in, k, chunk, idx, xs, sel, g_trace);
+  else if (C == 2) k_select<2><<<nseg, nt, sm, st>>>(x, d_in, k, chunk, idx, xs, sel, g_trace);
+  else k_select<4><<<nseg, nt, sm, st>>>(x, d_in, k, chunk, idx, xs, sel, g_trace);
   return cuda_status(cudaGetLastError());
 }
 
@@ -205,8 +238,9 @@ LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, 
   p.G = pl.G;
   p.row_bytes = L->d_in * L->w_bits / 8;
   p.TR = pl.TR;
-  p.RP = pl.RP;
-  p.RPT = pl.RPT;
+  p.NKW = pl.NKW;
+  p.NSLOTS = pl.NSLOTS;
+  p.RPS = pl.RPS;
   p.NC = pl.NC;
   p.stages = pl.stages;
   p.n_tiles = pl.n_tiles;
@@ -214,6 +248,8 @@ LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, 
   p.off_s = pl.off_s;
   p.off_z = pl.off_z;
   p.NGW = pl.NGW;
+  p.off_sel = pl.off_sel;
+  p.trace = g_trace ? g_trace + 2 : nullptr;
   return p;
 }
 
@@ -311,7 +347,11 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
     p.n_seg = (L->d_out + kSegCols - 1) / kSegCols;
     if (p.n_seg > kCntSlots) return DECDEC_EUNSUPPORTED;
     p.n_rb = (k_sel + kRB - 1) / kRB;
-    p.n_items = p.n_seg * p.n_rb;
+    const int ngw = P.pl.NGW * P.pl.grid;
+    int gws = ngw / p.n_seg;
+    if (gws < 1) gws = 1;
+    if (gws > p.n_rb) gws = p.n_rb;
+    p.gws = gws;
   }
   *out = P;
   return DECDEC_OK;
@@ -419,13 +459,19 @@ decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, si
   decdec_status s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &pl);
   if (s != DECDEC_OK) return s;
   snprintf(buf, buf_bytes,
-           "{\"G\": %d, \"RP\": %d, \"RPT\": %d, \"TR\": %d, \"NC\": %d, \"NGW\": %d, \"stages\": %d, "
-           "\"stage_bytes\": %u, \"n_tiles\": %d, \"grid\": %d, \"threads\": %d, \"smem\": %zu}",
-           pl.G, pl.RP, pl.RPT, pl.TR, pl.NC, pl.NGW, pl.stages, pl.stage_bytes, pl.n_tiles, pl.grid,
+           "{\"G\": %d, \"NKW\": %d, \"NSLOTS\": %d, \"RPS\": %d, \"TR\": %d, \"NC\": %d, \"NGW\": %d, "
+           "\"stages\": %d, \"stage_bytes\": %u, \"n_tiles\": %d, \"grid\": %d, \"threads\": %d, \"smem\": %zu}",
+           pl.G, pl.NKW, pl.NSLOTS, pl.RPS, pl.TR, pl.NC, pl.NGW, pl.stages, pl.stage_bytes, pl.n_tiles, pl.grid,
            32 * (1 + pl.NC + pl.NGW), pl.smem);
   return DECDEC_OK;
 }
 
 int32_t decdec_launches_per_call(int32_t k) { return k > 0 ? 2 : 1; }
+
+decdec_status decdec_debug_trace(void* buf, size_t bytes) {
+  if (buf && bytes < (size_t)(2 + 1024 * kTraceEvents) * 8) return DECDEC_ESPACE;
+  g_trace = static_cast<unsigned long long*>(buf);
+  return DECDEC_OK;
+}
 
 }  // extern "C"

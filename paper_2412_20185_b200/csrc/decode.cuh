@@ -9,6 +9,7 @@
 //   W3K: class 0 = offset 0 (x 2^-24), class 1 = offset 3 (x 2^-21), class 2 = offset 6 (x 2^-18)
 // The group sum is  sum q*x = 2^24 * (acc0 + acc1/16)            (4-bit)
 //                             2^24 * (acc0 + acc1/8 + acc2/64)    (3-bit)
+// (each class accumulator is split into a low-half and a high-half chain).
 #pragma once
 #include <cstdint>
 #include "ptx.cuh"
@@ -27,14 +28,16 @@ __device__ __forceinline__ void decode_w4_word(uint32_t w, uint32_t m[4]) {
 }
 __host__ __device__ constexpr int w4_class(int p) { return p & 1; }
 
-// acc[0..1] += codes(w) . x(xr[0..3]) for one 8-channel word; xr[p] = (x[2p], x[2p+1]).
+// acc[2c + h] += (half h of class-c codes) . x for one 8-channel word; xr[p] = (x[2p], x[2p+1]).
+// Low and high halves feed separate accumulators: 4 independent FHFMA chains per row.
 __device__ __forceinline__ void fma_w4_word(uint32_t w, const uint32_t* xr, float* acc) {
   uint32_t m[4];
   decode_w4_word(w, m);
-  acc[0] = fhfma2(m[0], xr[0], acc[0]);
-  acc[1] = fhfma2(m[1], xr[1], acc[1]);
-  acc[0] = fhfma2(m[2], xr[2], acc[0]);
-  acc[1] = fhfma2(m[3], xr[3], acc[1]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    acc[2 * w4_class(q)] = fhfma_lo(m[q], xr[q], acc[2 * w4_class(q)]);
+    acc[2 * w4_class(q) + 1] = fhfma_hi(m[q], xr[q], acc[2 * w4_class(q) + 1]);
+  }
 }
 
 // ---------------------------------------------------------------- W3K
@@ -61,12 +64,22 @@ __host__ __device__ constexpr int w3_class(int k) {
   return k == 15 ? 2 : ((k % 5) == 0 || (k % 5) == 3) ? 0 : ((k % 5) == 2 ? 2 : 1);
 }
 
-// acc[0..2] += codes(slice) . x(xr[0..15])
+// acc[2c + h] += (half h of class-c codes) . x(xr[0..15]): 6 independent FHFMA chains per row
 __device__ __forceinline__ void fma_w3_slice(uint32_t w0, uint32_t w1, uint32_t w2, const uint32_t* xr, float* acc) {
   uint32_t m[16];
   decode_w3_slice(w0, w1, w2, m);
 #pragma unroll
-  for (int k = 0; k < 16; ++k) acc[w3_class(k)] = fhfma2(m[k], xr[k], acc[w3_class(k)]);
+  for (int k = 0; k < 16; ++k) {
+    acc[2 * w3_class(k)] = fhfma_lo(m[k], xr[k], acc[2 * w3_class(k)]);
+    acc[2 * w3_class(k) + 1] = fhfma_hi(m[k], xr[k], acc[2 * w3_class(k) + 1]);
+  }
+}
+
+// Group sum of (q . x) in units of 2^-24, from the split accumulators.
+template <int BITS>
+__device__ __forceinline__ float combine_classes(const float* a) {
+  if (BITS == 4) return fmaf(a[2] + a[3], 0.0625f, a[0] + a[1]);
+  return fmaf(a[4] + a[5], 0.015625f, fmaf(a[2] + a[3], 0.125f, a[0] + a[1]));
 }
 
 // ---------------------------------------------------------------- Rq (residual, 4-bit)

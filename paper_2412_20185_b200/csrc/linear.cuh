@@ -6,16 +6,18 @@
 //   warp 0              producer: 1-D bulk async copies (TMA engine, cp.async.bulk) of
 //                       TR packed rows + their scales/zeros into a `stages`-deep smem ring
 //                       (mbarrier full/empty pairs), L2 evict-first.
-//   warps 1..NC         consumers: thread (g, rp) owns input group g (128 channels, x kept
-//                       in 64 registers for the whole launch) and row phase rp; decodes
-//                       codes in registers (decode.cuh), FHFMA fp32 accumulation, applies
-//                       the group's z and s, writes a partial per (row, group) to smem; one
-//                       named barrier per tile, then a fixed-order warp reduction per row.
+//   warps 1..NC         consumers: a thread owns input group g (128 channels, x kept in 64
+//                       registers for the whole launch) and a row slot; per tile it computes
+//                       RPS rows, two at a time (6-8 independent FHFMA chains), decoding codes
+//                       in registers (decode.cuh), fp32 accumulation, then the group's z, s.
+//                       G | 32: a warp holds 32/G whole rows -> shuffle reduction only;
+//                       else NKW warps per row -> shuffle + one named barrier per team/tile.
 //   warps NC+1..NC+NGW  gather warps (only when k > 0): wait for the selector kernel
-//                       (programmatic dependent launch), then stream residual rows
-//                       R_hat[S, 256-column segment] from pinned host memory with zero-copy
-//                       loads, RB rows in flight per warp, decode + FHFMA, write a
-//                       per-row-block partial.  Work item = (segment, row block).
+//                       (programmatic dependent launch), stage S and x[S] in smem, then for
+//                       work item (256-column segment, j) stream row blocks j, j+gws, ... of
+//                       R_hat[S, segment] from pinned host memory with zero-copy loads
+//                       (P:251), double-buffered (16 rows in flight per warp), decode + FHFMA,
+//                       one fp32 partial per item.
 // Combine (P:207 step 4; the paper uses atomics): every producer of a 256-column
 // segment (GEMV rows, gather row blocks) publishes with a fence and bumps the segment's
 // arrival counter; the last arriver sums  y = fp16(o_b + S_j * sum_rb part_rb)  in a fixed
@@ -23,6 +25,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
+#include <type_traits>
 #include "ptx.cuh"
 #include "decode.cuh"
 
@@ -31,7 +34,15 @@ namespace decdec {
 constexpr int kRB = 8;            // residual rows per gather work item (in flight per lane)
 constexpr int kSegCols = 256;     // output columns per combine segment (128 B of 4-bit codes)
 constexpr int kMaxThreads = 480;  // 1 producer + <= 12 consumer + 2 gather warps
+constexpr int kMaxRPS = 4;       // rows per slot per tile
 constexpr int kCntSlots = 4096;   // arrival counters at the head of the workspace
+// trace events (per CTA): 0 start, 1 first TMA issued, 2 x loaded, 3 first stage landed,
+// 4 GEMV done, 5 selector visible, 6 selection staged, 7 gather done, 8 consumer exit
+constexpr int kTraceEvents = 9;
+#define DECDEC_TRACE(p, ev)                                                        \
+  do {                                                                             \
+    if ((p).trace) (p).trace[blockIdx.x * kTraceEvents + (ev)] = globaltimer();    \
+  } while (0)
 
 struct LinearParams {
   const uint8_t* w;      // packed weights (W3K/W4K), [d_out][row_bytes]
@@ -40,7 +51,10 @@ struct LinearParams {
   const uint16_t* x;     // fp16 [d_in]
   uint16_t* y;           // fp16 [d_out]
   int d_in, d_out, G, row_bytes;
-  int TR, RP, RPT, NC, stages, n_tiles;
+  int TR, NC, stages, n_tiles;
+  int NKW;     // warps per row team; 0 = a warp holds 32/G whole rows (G divides 32)
+  int NSLOTS;  // concurrent row slots per CTA: NC*32/G (G <= 32) or NC/NKW (G > 32)
+  int RPS;     // rows per slot per tile (TR = NSLOTS * RPS)
   uint32_t stage_bytes, off_s, off_z;
   // compensation (k_sel == 0: none)
   int k_sel;
@@ -53,7 +67,9 @@ struct LinearParams {
   float* part;
   uint16_t* sdev;
   uint32_t* cnt;
-  int n_seg, n_rb, n_items, NGW;
+  int n_seg, n_rb, gws, NGW;  // gws = gather warps per segment (each takes row blocks j, j+gws, ...)
+  uint32_t off_sel;            // smem offset of the staged selection (idx int32[k], xs u16[k])
+  unsigned long long* trace;   // optional per-CTA event timestamps [grid][kTraceEvents] (ns), or null
 };
 
 template <int RBITS>
@@ -62,8 +78,8 @@ __device__ __forceinline__ void combine_segment(const LinearParams& p, int seg, 
   if (col0 >= p.d_out) return;
   const float4 o0 = ld_cg_f4(p.ob + col0), o1 = ld_cg_f4(p.ob + col0 + 4);
   float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int rb = 0; rb < p.n_rb; ++rb) {  // fixed order: row blocks ascending
-    const float* pp = p.part + (size_t)rb * p.d_out + col0;
+  for (int j = 0; j < p.gws; ++j) {  // fixed order: gather warps of the segment ascending
+    const float* pp = p.part + (size_t)j * p.d_out + col0;
     const float4 a = ld_cg_f4(pp), b = ld_cg_f4(pp + 4);
     s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
     s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
@@ -98,7 +114,7 @@ __device__ __forceinline__ void arrive_segment(const LinearParams& p, int seg, u
   if (lane == 0) old = atomicAdd(p.cnt + seg, add);
   old = __shfl_sync(0xffffffffu, old, 0);
   const int seg_cols = min(kSegCols, p.d_out - seg * kSegCols);
-  if (old + add == (uint32_t)(seg_cols + p.n_rb)) {
+  if (old + add == (uint32_t)(seg_cols + p.gws)) {
     __threadfence();
     combine_segment<RBITS>(p, seg, lane);
     if (lane == 0) p.cnt[seg] = 0;  // ready for the next call
@@ -109,8 +125,8 @@ template <int BITS, int RBITS>
 __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stage0 = smem;
-  float* red = reinterpret_cast<float*>(smem + (size_t)p.stages * p.stage_bytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * p.TR * p.G);
+  float* red = reinterpret_cast<float*>(smem + (size_t)p.stages * p.stage_bytes);  // [2][NSLOTS][4][NKW]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * p.NSLOTS * 4 * max(p.NKW, 1));
   uint64_t* empty = full + p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -122,6 +138,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     fence_mbar_init();
   }
   __syncthreads();
+  if (threadIdx.x == 0) DECDEC_TRACE(p, 0);
 
   // ------------------------------------------------------------------ producer (TMA)
   if (warp == 0) {
@@ -137,6 +154,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
         bulk_g2s(dst, p.w + (size_t)tile * wb, wb, &full[st], pol);
         bulk_g2s(dst + p.off_s, p.ws + (size_t)tile * p.TR * p.G, sb, &full[st], pol);
         bulk_g2s(dst + p.off_z, p.wz + (size_t)tile * p.TR * p.G, zb, &full[st], pol);
+        if (it == 0) DECDEC_TRACE(p, 1);
       }
     }
     return;
@@ -146,9 +164,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
   if (warp <= p.NC) {
     constexpr int GB = 16 * BITS;  // bytes of one 128-code group
     const int ct = threadIdx.x - 32;
+    const int cw = ct >> 5;
     const int G = p.G;
-    const int g = ct % G, rp = ct / G;
-    const bool active = rp < p.RP;
+    const bool small_g = p.NKW == 0;  // a warp holds 32/G whole rows (G | 32); else NKW warps per row
+    const int g = small_g ? (lane % G) : ((cw % p.NKW) * 32 + lane);
+    const int slot = small_g ? (cw * (32 / G) + lane / G) : (cw / max(p.NKW, 1));
+    const bool active = g < G;
     const int rot = (BITS == 4) ? ((g >> 1) & 3) : 0;  // 4-bit: bank-conflict-free 16-B chunk order
     uint32_t xr[64];
     float Xs = 0.f;
@@ -172,102 +193,207 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
         Xs += __half2float(__ushort_as_half((unsigned short)(xr[i] >> 16)));
       }
       Xs *= 5.9604644775390625e-08f;  // 2^-24: same scale as the decoded codes
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) xr[i] = 0u;
     }
-    const int cw = warp - 1;
+    if (ct == 0) {
+      asm volatile("" ::"f"(Xs));  // order the timestamp after x has landed
+      DECDEC_TRACE(p, 2);
+    }
+    const int nkw = small_g ? 1 : p.NKW;
+    const int team = cw / nkw, wi = cw % nkw;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
       const int st = it % p.stages;
       mbar_wait(&full[st], (it / p.stages) & 1);
+      if (it == 0 && ct == 0) DECDEC_TRACE(p, 3);
       const uint8_t* sw = stage0 + (size_t)st * p.stage_bytes;
       const uint16_t* ss = reinterpret_cast<const uint16_t*>(sw + p.off_s);
       const uint8_t* sz = sw + p.off_z;
-      float* rbuf = red + (it & 1) * p.TR * G;
-      if (active) {
-        for (int m = 0; m < p.RPT; ++m) {
-          const int r = rp + m * p.RP;
-          const uint8_t* gp = sw + (size_t)r * p.row_bytes + g * GB;
-          float acc[3] = {0.f, 0.f, 0.f};
+      float part[4] = {0.f, 0.f, 0.f, 0.f};  // RPS <= 4
+#pragma unroll
+      for (int m = 0; m < kMaxRPS; m += 2) {
+        if (m >= p.RPS) break;
+        const bool two = m + 1 < p.RPS;
+        const int r0 = slot + m * p.NSLOTS, r1 = slot + (m + 1) * p.NSLOTS;
+        if (active) {
+          const uint8_t* g0 = sw + (size_t)r0 * p.row_bytes + g * GB;
+          const uint8_t* g1 = sw + (size_t)(two ? r1 : r0) * p.row_bytes + g * GB;
+          float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, a1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
           if (BITS == 4) {
+            uint4 v0[4], v1[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const uint4 v = *reinterpret_cast<const uint4*>(gp + 16 * ((j + rot) & 3));
-              fma_w4_word(v.x, xr + 16 * j + 0, acc);
-              fma_w4_word(v.y, xr + 16 * j + 4, acc);
-              fma_w4_word(v.z, xr + 16 * j + 8, acc);
-              fma_w4_word(v.w, xr + 16 * j + 12, acc);
+              v0[j] = *reinterpret_cast<const uint4*>(g0 + 16 * ((j + rot) & 3));
+              v1[j] = *reinterpret_cast<const uint4*>(g1 + 16 * ((j + rot) & 3));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              fma_w4_word(v0[j].x, xr + 16 * j + 0, a0);
+              fma_w4_word(v1[j].x, xr + 16 * j + 0, a1);
+              fma_w4_word(v0[j].y, xr + 16 * j + 4, a0);
+              fma_w4_word(v1[j].y, xr + 16 * j + 4, a1);
+              fma_w4_word(v0[j].z, xr + 16 * j + 8, a0);
+              fma_w4_word(v1[j].z, xr + 16 * j + 8, a1);
+              fma_w4_word(v0[j].w, xr + 16 * j + 12, a0);
+              fma_w4_word(v1[j].w, xr + 16 * j + 12, a1);
             }
           } else {
-            const uint4 v0 = *reinterpret_cast<const uint4*>(gp);
-            const uint4 v1 = *reinterpret_cast<const uint4*>(gp + 16);
-            const uint4 v2 = *reinterpret_cast<const uint4*>(gp + 32);
-            const uint32_t wv[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+            uint32_t w0[12], w1[12];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) fma_w3_slice(wv[3 * u], wv[3 * u + 1], wv[3 * u + 2], xr + 16 * u, acc);
+            for (int j = 0; j < 3; ++j) {
+              const uint4 t0 = *reinterpret_cast<const uint4*>(g0 + 16 * j);
+              const uint4 t1 = *reinterpret_cast<const uint4*>(g1 + 16 * j);
+              w0[4 * j] = t0.x; w0[4 * j + 1] = t0.y; w0[4 * j + 2] = t0.z; w0[4 * j + 3] = t0.w;
+              w1[4 * j] = t1.x; w1[4 * j + 1] = t1.y; w1[4 * j + 2] = t1.z; w1[4 * j + 3] = t1.w;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              fma_w3_slice(w0[3 * u], w0[3 * u + 1], w0[3 * u + 2], xr + 16 * u, a0);
+              fma_w3_slice(w1[3 * u], w1[3 * u + 1], w1[3 * u + 2], xr + 16 * u, a1);
+            }
           }
-          const float sc = __half2float(__ushort_as_half(ss[r * G + g])) * 16777216.f;  // s * 2^24
-          const float zf = (float)sz[r * G + g];
-          const float t = (BITS == 4) ? fmaf(acc[1], 0.0625f, acc[0])
-                                      : fmaf(acc[2], 0.015625f, fmaf(acc[1], 0.125f, acc[0]));
-          rbuf[r * G + g] = sc * fmaf(-zf, Xs, t);  // s * sum_(i in g) (q_i - z) x_i
+          const float t0 = combine_classes<BITS>(a0);
+          const float t1 = combine_classes<BITS>(a1);
+          const float s0 = __half2float(__ushort_as_half(ss[r0 * G + g])) * 16777216.f;  // s * 2^24
+          const float z0 = (float)sz[r0 * G + g];
+          part[m] = s0 * fmaf(-z0, Xs, t0);  // s * sum_(i in g) (q_i - z) x_i
+          if (two) {
+            const float s1 = __half2float(__ushort_as_half(ss[r1 * G + g])) * 16777216.f;
+            const float z1 = (float)sz[r1 * G + g];
+            part[m + 1] = s1 * fmaf(-z1, Xs, t1);
+          }
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);  // stage fully read into registers
-      named_bar_sync(1, p.NC * 32);
+      if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done reading the stage
       int nrows = 0;
-      for (int r = cw; r < p.TR; r += p.NC) {
-        float s = 0.f;
-        for (int gg = lane; gg < G; gg += 32) s += rbuf[r * G + gg];
+      if (small_g) {
+        // rows are whole inside the warp: butterfly over the G lanes of each row (fixed order)
 #pragma unroll
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        const int row = tile * p.TR + r;
-        if (lane == 0) {
-          if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(s));
-          else p.ob[row] = s;
+        if (G == 32 && p.RPS == 4) {
+          // transposed butterfly: 4 rows in 6 shuffles / 5 dependent rounds (fixed order)
+          const bool hi16 = lane & 16, hi8 = lane & 8;
+          float u0 = (hi16 ? part[2] : part[0]) + __shfl_xor_sync(0xffffffffu, hi16 ? part[0] : part[2], 16);
+          float u1 = (hi16 ? part[3] : part[1]) + __shfl_xor_sync(0xffffffffu, hi16 ? part[1] : part[3], 16);
+          float v = (hi8 ? u1 : u0) + __shfl_xor_sync(0xffffffffu, hi8 ? u0 : u1, 8);
+#pragma unroll
+          for (int o = 4; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if ((lane & 7) == 0) {  // lane 0 -> row 0, 8 -> 1, 16 -> 2, 24 -> 3
+            const int m = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
+            const int row = tile * p.TR + slot + m * p.NSLOTS;
+            if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
+            else p.ob[row] = v;
+          }
+        } else if (G == 32 && p.RPS == 2) {
+          const bool hi16 = lane & 16;
+          float v = (hi16 ? part[1] : part[0]) + __shfl_xor_sync(0xffffffffu, hi16 ? part[0] : part[1], 16);
+#pragma unroll
+          for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if ((lane & 15) == 0) {
+            const int row = tile * p.TR + slot + (hi16 ? 1 : 0) * p.NSLOTS;
+            if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
+            else p.ob[row] = v;
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < kMaxRPS; ++m) {
+            if (m >= p.RPS) break;
+            float v = part[m];
+            for (int o = G >> 1; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (g == 0) {
+              const int row = tile * p.TR + slot + m * p.NSLOTS;
+              if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
+              else p.ob[row] = v;
+            }
+          }
         }
-        ++nrows;
+        nrows = p.RPS * (32 / G);
+      } else {
+        // NKW warps per row: warp butterfly, then the team's first warp sums the NKW partials
+        float* rbuf = red + ((it & 1) * p.NSLOTS + team) * 4 * p.NKW;
+#pragma unroll
+        for (int m = 0; m < kMaxRPS; ++m) {
+          if (m >= p.RPS) break;
+          float v = part[m];
+#pragma unroll
+          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0) rbuf[m * p.NKW + wi] = v;
+        }
+        named_bar_sync(1 + team, p.NKW * 32);
+        if (wi == 0) {
+          if (lane < p.RPS) {
+            float v = 0.f;
+            for (int w = 0; w < p.NKW; ++w) v += rbuf[lane * p.NKW + w];
+            const int row = tile * p.TR + slot + lane * p.NSLOTS;
+            if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
+            else p.ob[row] = v;
+          }
+          nrows = p.RPS;
+        }
       }
       if (p.k_sel > 0 && nrows > 0) {
         __threadfence();
         arrive_segment<RBITS>(p, (tile * p.TR) / kSegCols, (uint32_t)nrows, lane);
       }
     }
+    if (ct == 0) DECDEC_TRACE(p, 4);
     return;
   }
 
   // ------------------------------------------------------------------ gather warps (DEC)
   if (p.k_sel <= 0) return;
+  const int gwi = warp - 1 - p.NC;
+  int* sidx = reinterpret_cast<int*>(smem + p.off_sel);
+  uint16_t* sxs = reinterpret_cast<uint16_t*>(sidx + p.k_sel);
   pdl_wait();  // selector kernel complete and its writes visible
-  const int gw = (warp - 1 - p.NC) + p.NGW * blockIdx.x, ngw = p.NGW * gridDim.x;
-  for (int item = gw; item < p.n_items; item += ngw) {
-    const int seg = item % p.n_seg, rbk = item / p.n_seg;
-    const int r0 = rbk * kRB, nr = min(kRB, p.k_sel - r0);
+  if (gwi == 0 && lane == 0) DECDEC_TRACE(p, 5);
+  for (int i = gwi * 32 + lane; i < p.k_sel; i += p.NGW * 32) {
+    sidx[i] = __ldcg(p.idx + i);
+    sxs[i] = __ldcg(p.xs + i);
+  }
+  named_bar_sync(15, p.NGW * 32);
+  if (gwi == 0 && lane == 0) DECDEC_TRACE(p, 6);
+  const int gw = gwi + p.NGW * blockIdx.x, ngw = p.NGW * gridDim.x;
+  for (int pair = gw; pair < p.n_seg * p.gws; pair += ngw) {
+    const int seg = pair % p.n_seg, j = pair / p.n_seg;
     const int col0 = seg * kSegCols + lane * 8;
     const bool cv = col0 < p.d_out;
-    int myrow = 0;
-    uint32_t myxs = 0;
-    if (lane < nr) {
-      myrow = __ldcg(p.idx + r0 + lane);
-      myxs = __ldcg(p.xs + r0 + lane);
+    if (RBITS == 4 && j == 0 && cv) {  // all scale factors are fetched every call
+      const uint4 sv = ld_zc_u4(p.r_scales + col0);
+      *reinterpret_cast<uint4*>(p.sdev + col0) = sv;
     }
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (RBITS == 4) {
-      uint32_t wv[kRB];
+    // row blocks rb = j, j + gws, ... (8 rows each), double-buffered: next block's zero-copy
+    // loads are in flight while the current block is decoded.
+    using Vec = typename std::conditional<RBITS == 4, uint32_t, uint4>::type;
+    auto load = [&](int rb, Vec* buf) {
 #pragma unroll
       for (int r = 0; r < kRB; ++r) {
-        const int row = __shfl_sync(0xffffffffu, myrow, r);
-        wv[r] = (r < nr && cv) ? ld_zc_u32(p.r_rows + (size_t)row * p.r_row_bytes + (col0 >> 1)) : 0u;
+        const int e = rb * kRB + r;
+        if (e < p.k_sel && cv) {
+          const uint8_t* rowp = p.r_rows + (size_t)sidx[e] * p.r_row_bytes;
+          if constexpr (RBITS == 4) buf[r] = ld_zc_u32(rowp + (col0 >> 1));
+          else buf[r] = ld_zc_u4(rowp + col0 * 2);
+        } else {
+          if constexpr (RBITS == 4) buf[r] = 0u;
+          else buf[r] = make_uint4(0, 0, 0, 0);
+        }
       }
-      if (rbk == 0 && cv) {  // all scale factors are fetched every call
-        const uint4 sv = ld_zc_u4(p.r_scales + col0);
-        *reinterpret_cast<uint4*>(p.sdev + col0) = sv;
-      }
+    };
+    auto consume = [&](int rb, const Vec* buf) {
 #pragma unroll
       for (int r = 0; r < kRB; ++r) {
-        const uint16_t xv = (uint16_t)__shfl_sync(0xffffffffu, myxs, r);
-        if (r < nr) {
+        const int e = rb * kRB + r;
+        if (e < p.k_sel) {
+          const uint16_t xv = sxs[e];
           uint32_t c[4];
-          decode_rq_word(wv[r], c);
+          if constexpr (RBITS == 4) {
+            decode_rq_word(buf[r], c);
+          } else {
+            c[0] = buf[r].x; c[1] = buf[r].y; c[2] = buf[r].z; c[3] = buf[r].w;
+          }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             acc[2 * q] = fhfma_s_lo(xv, c[q], acc[2 * q]);
@@ -275,34 +401,29 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
           }
         }
       }
-    } else {
-      uint4 wv[kRB];
-#pragma unroll
-      for (int r = 0; r < kRB; ++r) {
-        const int row = __shfl_sync(0xffffffffu, myrow, r);
-        wv[r] = (r < nr && cv) ? ld_zc_u4(p.r_rows + (size_t)row * p.r_row_bytes + col0 * 2) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int r = 0; r < kRB; ++r) {
-        const uint16_t xv = (uint16_t)__shfl_sync(0xffffffffu, myxs, r);
-        if (r < nr) {
-          const uint32_t h[4] = {wv[r].x, wv[r].y, wv[r].z, wv[r].w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            acc[2 * q] = fhfma_s_lo(xv, h[q], acc[2 * q]);
-            acc[2 * q + 1] = fhfma_s_hi(xv, h[q], acc[2 * q + 1]);
-          }
-        }
-      }
+    };
+    Vec bufA[kRB], bufB[kRB];
+    int rb = j;
+    load(rb, bufA);
+    while (true) {
+      if (rb + p.gws < p.n_rb) load(rb + p.gws, bufB);
+      consume(rb, bufA);
+      rb += p.gws;
+      if (rb >= p.n_rb) break;
+      if (rb + p.gws < p.n_rb) load(rb + p.gws, bufA);
+      consume(rb, bufB);
+      rb += p.gws;
+      if (rb >= p.n_rb) break;
     }
     if (cv) {
-      float* pp = p.part + (size_t)rbk * p.d_out + col0;
+      float* pp = p.part + (size_t)j * p.d_out + col0;
       *reinterpret_cast<float4*>(pp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
       *reinterpret_cast<float4*>(pp + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
     __threadfence();
     arrive_segment<RBITS>(p, seg, 1u, lane);
   }
+  if (gwi == 0 && lane == 0) DECDEC_TRACE(p, 7);
 }
 
 // Debug: decode packed weights with the kernel's own decode path; q_out u8 [d_out][d_in].

@@ -103,4 +103,11 @@ __device__ __forceinline__ uint4 ld_zc_u4(const void* p) {
   return v;
 }
 
+// ---------------------------------------------------------------- tracing (debug timelines)
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 }  // namespace decdec
