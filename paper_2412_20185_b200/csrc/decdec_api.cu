@@ -136,9 +136,9 @@ decdec_status g_attr_status = DECDEC_OK;
 void init_attrs() {
   decdec_status s = DECDEC_OK;
   const size_t lin = 227 * 1024;
-  if (s == DECDEC_OK) s = set_smem_attr(k_select<1>, 160 * 1024);
-  if (s == DECDEC_OK) s = set_smem_attr(k_select<2>, 160 * 1024);
-  if (s == DECDEC_OK) s = set_smem_attr(k_select<4>, 160 * 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_select<1>, 132 * 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_select<2>, 132 * 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_select<4>, 132 * 1024);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 16>, lin);
@@ -199,7 +199,7 @@ decdec_status launch_select(const uint16_t* x, int d_in, int k, int chunk, int* 
   int nt = 32, C = 1;
   select_geometry(n, &nt, &C);
   const int nseg = chunk ? (d_in + chunk - 1) / chunk : 1;
-  const size_t sm = select_smem_bytes(nt, n);
+  const size_t sm = select_smem_bytes();
   if (C == 1) k_select<1><<<nseg, nt, sm, st>>>(x, d_in, k, chunk, idx, xs, sel, g_trace);
   else if (C == 2) k_select<2><<<nseg, nt, sm, st>>>(x, d_in, k, chunk, idx, xs, sel, g_trace);
   else k_select<4><<<nseg, nt, sm, st>>>(x, d_in, k, chunk, idx, xs, sel, g_trace);

@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     }
     const int nkw = small_g ? 1 : p.NKW;
     const int team = cw / nkw, wi = cw % nkw;
+    int nrows_tile = 0;  // o_b rows this warp writes per tile (same for every tile)
     int it = 0;
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
       const int st = it % p.stages;
@@ -333,12 +334,16 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
           nrows = p.RPS;
         }
       }
-      if (p.k_sel > 0 && nrows > 0) {
-        __threadfence();
-        arrive_segment<RBITS>(p, (tile * p.TR) / kSegCols, (uint32_t)nrows, lane);
-      }
+      nrows_tile = nrows;
     }
     if (ct == 0) DECDEC_TRACE(p, 4);
+    // Publish o_b rows once per warp (one fence for all tiles, then one arrival per tile):
+    // a fence per tile stalled the GEMV stream by ~1 µs each.
+    if (p.k_sel > 0 && nrows_tile > 0) {
+      __threadfence();
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x)
+        arrive_segment<RBITS>(p, (tile * p.TR) / kSegCols, (uint32_t)nrows_tile, lane);
+    }
     return;
   }
 
@@ -420,10 +425,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       *reinterpret_cast<float4*>(pp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
       *reinterpret_cast<float4*>(pp + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
-    __threadfence();
-    arrive_segment<RBITS>(p, seg, 1u, lane);
   }
   if (gwi == 0 && lane == 0) DECDEC_TRACE(p, 7);
+  __threadfence();  // one fence for all of this warp's partials, then the arrivals
+  for (int pair = gw; pair < p.n_seg * p.gws; pair += ngw) arrive_segment<RBITS>(p, pair % p.n_seg, 1u, lane);
 }
 
 // Debug: decode packed weights with the kernel's own decode path; q_out u8 [d_out][d_in].

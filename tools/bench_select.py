@@ -61,4 +61,4 @@ for d_in in (1024, 4096, 14336):
     c0 = t[2 + 1024 * 9 - 2]
     ph = [int(t[2 + 1024 * 9 - 16 + i] - c0) for i in range(6)]
     print(d_in, "select us (start->end):", round((t[1] - t0) / 1e3, 2), "cycles", cyc, "=> MHz", round(cyc / ((t[1] - t0) / 1e3)),
-          "phase cycles staged/l1tot/b1/cand/T/scan:", ph)
+          "phase cycles zeroed/hist/T/scan:", ph[:4])
