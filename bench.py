@@ -1,13 +1,15 @@
 #!/usr/bin/env python
 """DecDEC decode-step benchmark (BASELINE.json metric: µs per decode linear layer & tokens/s vs
 k_chunk; % of HBM+PCIe roofline), workload BASELINE.json configs[1]: Llama-3-8B decode, all
-q/k/v/o/gate/up/down shapes x 32 blocks, 3-bit W_hat (group 128) + 4-bit residual in pinned host
+q/k/v/o/gate/up/down weights x 32 blocks, 3-bit W_hat (group 128) + 4-bit residual in pinned host
 memory, exact Top-k per layer per step on outlier-heavy synthetic activations.
 
-A "step" = one decode step's whole linear stack (224 layer calls, each = exact Top-k selector +
-fused GEMV/zero-copy-gather/combine kernel), replayed as one native CUDA graph
-(decdec_stack_*).  Inputs are resident in HBM when the timed region starts; the step streams
-2.8 GB of packed weights (> 126 MB L2), so no L2 flush is needed.
+A "step" = one decode step's whole linear stack, called per the paper's layer classes qkv, o, gu,
+d (q/k/v share x and so do gate/up, so they are one GEMV each) -- 128 layer calls, each =
+exact Top-k selector + fused GEMV/zero-copy-gather/combine kernel -- replayed as one native CUDA
+graph (decdec_stack_*), consecutive layers chained by programmatic dependent launch.
+(--unfused: 224 separate q/k/v/o/gate/up/down calls.)  Inputs are resident in HBM when the timed
+region starts; the step streams 2.8 GB of packed weights (> 126 MB L2), so no L2 flush is needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--kchunk 21] [--sweep 0,8,21]
   python bench.py --impl reference ...      # the float64 CPU oracle, timed on host cores
@@ -121,10 +123,10 @@ class ClockSampler:
 class Model:
     """Llama-3-8B (or another model) decode linear stack on this rank."""
 
-    def __init__(self, dd, torch, model, bits, rank, world, n_x_sets, device):
+    def __init__(self, dd, torch, model, bits, rank, world, n_x_sets, device, fused=True):
         self.layers, self.meta = [], []  # meta: (block, name, d_in, d_out_shard)
         self.hosts = []
-        shapes = model_layers(model, fused=False) if model == "llama3_8b" else model_layers(model, fused=True)
+        shapes = model_layers(model, fused=fused)
         self.n_blocks = MODEL_BLOCKS[model]
         for b in range(self.n_blocks):
             for name, d_in, d_out in shapes:
@@ -192,12 +194,12 @@ def time_graphs(torch, dist, launches, K, W, stream, world):
     return ms
 
 
-def cpu_oracle_block(model, bits, kc, seed_tag="cpu"):
+def cpu_oracle_block(model, bits, kc, fused=True, seed_tag="cpu"):
     """Time the oracle (as it stands) on one decoder block's layers (a bounded sample)."""
     import oracle
     from synth import gen_perf_layer
 
-    shapes = model_layers(model, fused=False) if model == "llama3_8b" else model_layers(model, fused=True)
+    shapes = model_layers(model, fused=fused)
     data = []
     for name, d_in, d_out in shapes:
         L = gen_perf_layer(d_in, d_out, bits, seed=layer_seed(seed_tag, name))
@@ -229,7 +231,7 @@ def run_reference(args, rank, world):
     from synth import gen_perf_layer
 
     model, bits, kc = args.model, args.bits, args.kchunk
-    shapes = model_layers(model, fused=False) if model == "llama3_8b" else model_layers(model, fused=True)
+    shapes = model_layers(model, fused=not args.unfused)
     data = []
     for name, d_in, d_out in shapes:
         L = gen_perf_layer(d_in, d_out, bits, seed=layer_seed("ref", name))
@@ -286,6 +288,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nx", type=int, default=4, help="distinct activation sets cycled across steps")
     ap.add_argument("--quick", action="store_true", help="headline step only (for ncu launch lists)")
+    ap.add_argument("--unfused", action="store_true",
+                    help="7 separate q/k/v/o/gate/up/down calls per block instead of the paper's layer "
+                         "classes qkv, o, gu, d (P:304); per-layer µs of the 7 shapes are reported either way")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -308,7 +313,7 @@ def main():
     hbm_peak, hbm_src, pcie_peak, pcie_src = load_peaks()
 
     t_build = time.time()
-    M = Model(dd, torch, args.model, args.bits, rank, world, args.nx, dev)
+    M = Model(dd, torch, args.model, args.bits, rank, world, args.nx, dev, fused=not args.unfused)
     sweep = sorted({int(v) for v in args.sweep.split(",") if v != ""} | {args.kchunk})
     if args.quick:
         sweep, args.no_cpu_baseline = [args.kchunk], True
@@ -443,7 +448,7 @@ def main():
     # ---- CPU baseline (oracle on host cores, rank 0, N = 1) ----------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times = cpu_oracle_block(args.model, args.bits, args.kchunk)
+        times = cpu_oracle_block(args.model, args.bits, args.kchunk, fused=not args.unfused)
         blk = sum(times.values())
         cpu = {"value": 1.0 / (M.n_blocks * blk), "unit": "tokens/s", "cores": blas_threads(), "kind": "oracle",
                "sample": f"one decoder block ({', '.join(times)}) through oracle.decdec_linear_ref at "
@@ -457,7 +462,8 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": f"int{args.bits} weights x f16 activations -> f32 accumulate (f16 out); int4 residual",
             "data": "synthetic (seeded; random packed codes, outlier-heavy Student-t activations)",
-            "config": {"workload": f"{args.model} decode linear stack: {n_layers // M.n_blocks} layers x "
+            "config": {"workload": f"{args.model} decode linear stack: {n_layers // M.n_blocks} layer calls "
+                                   f"({'q,k,v,o,gate,up,down' if args.unfused else 'qkv,o,gu,d classes, P:304'}) x "
                                    f"{M.n_blocks} blocks, w{args.bits} g128, r4 residual in pinned host memory, "
                                    f"exact Top-k, k_chunk={args.kchunk}",
                        "k_chunk": args.kchunk, "layers_per_step": n_layers,

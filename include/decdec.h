@@ -162,15 +162,16 @@ decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out,
                                           decdec_stream_t stream);
 
 /* Debug timelines: while buf != NULL every launch records %globaltimer (ns) events into buf
- * (u64: [0] selector start, [1] selector end, then per CTA 9 events: start, first bulk copy
- * issued, x loaded, first stage landed, GEMV done, selector visible, selection staged, gather
- * done).  bytes >= (2 + 1024*9)*8.  Not thread-safe; NULL disables (default). */
+ * (u64: [0..1] unused, then per CTA 9 events: start, first bulk copy issued, x loaded, first
+ * stage landed, GEMV done, selector start / selection staged, selection published, gather
+ * done; selector CTAs come first).  bytes >= (2 + 1024*9)*8.  Not thread-safe; NULL disables. */
 decdec_status decdec_debug_trace(void* buf, size_t bytes);
 
 /* Launch plan chosen for a layer (tile rows, consumer warps, stages, grid) as text. */
 decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, size_t buf_bytes);
 
-/* Number of kernels decdec_linear enqueues for (k): 2 when k > 0 (select + fused), else 1. */
+/* Number of kernels decdec_linear enqueues for (k): always 1 (the selector runs on the fused
+ * kernel's first CTA(s)). */
 int32_t decdec_launches_per_call(int32_t k);
 
 const char* decdec_status_string(decdec_status s);

@@ -46,7 +46,8 @@ constexpr size_t kSmemBudget = 200 * 1024;
 // Launch plan: enumerate (consumer warps NC, rows per slot RPS); pick the one minimising the
 // busiest CTA's bytes (ceil(tiles / SMs) x (stage bytes + a per-tile overhead equivalent)),
 // ties -> more consumer warps.  DECDEC_PLAN="NC,RPS" overrides (tuning).
-decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl) {
+decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int sel_ctas = 1, int sel_len = 0) {
+  if (sel_len == 0) sel_len = d_in;
   const int G = d_in / DECDEC_GROUP;
   const int sms = device_sms();
   const bool small_g = G <= 32 && 32 % G == 0;
@@ -84,12 +85,13 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl) {
       if (p.stages > 8) p.stages = 8;
       if (p.stages < 2) continue;
       p.n_tiles = d_out / p.TR;
-      // k > 0: leave one SM free for the selector kernel that runs concurrently (PDL)
-      const int max_grid = k_sel > 0 ? sms - 1 : sms;
+      // k > 0: the selector CTA(s) take the first SMs; GEMV CTAs fill the rest
+      const int max_grid = k_sel > 0 ? sms - sel_ctas : sms;
       p.grid = p.n_tiles < max_grid ? p.n_tiles : max_grid;
       p.NGW = k_sel > 0 ? 2 : 0;
       p.off_sel = (uint32_t)((size_t)p.stages * p.stage_bytes + red + (size_t)2 * p.stages * 8);
       p.smem = p.off_sel + sel;
+      if (k_sel > 0 && p.smem < select_block_smem_bytes(sel_len)) p.smem = select_block_smem_bytes(sel_len);
       const double waves = (double)((p.n_tiles + sms - 1) / sms);
       const double cost = waves * ((double)p.stage_bytes + 3072.0) * (nc < 4 ? 1.0 + 0.15 * (4 - nc) : 1.0);
       if (!have || cost < best_cost * 0.999 || (cost <= best_cost * 1.001 && p.NC > best.NC)) {
@@ -135,10 +137,8 @@ std::once_flag g_attr_once;
 decdec_status g_attr_status = DECDEC_OK;
 void init_attrs() {
   decdec_status s = DECDEC_OK;
-  const size_t lin = 227 * 1024;
-  if (s == DECDEC_OK) s = set_smem_attr(k_select<1>, 132 * 1024);
-  if (s == DECDEC_OK) s = set_smem_attr(k_select<2>, 132 * 1024);
-  if (s == DECDEC_OK) s = set_smem_attr(k_select<4>, 132 * 1024);
+  const size_t lin = 226 * 1024;  // + static smem <= 227 KB
+  if (s == DECDEC_OK) s = set_smem_attr(k_select, 80 * 1024);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 16>, lin);
@@ -196,13 +196,10 @@ int n_selected(int d_in, int k, int chunk) {
 decdec_status launch_select(const uint16_t* x, int d_in, int k, int chunk, int* idx, uint16_t* xs, int* sel,
                             cudaStream_t st) {
   const int n = chunk ? (chunk < d_in ? chunk : d_in) : d_in;
-  int nt = 32, C = 1;
-  select_geometry(n, &nt, &C);
   const int nseg = chunk ? (d_in + chunk - 1) / chunk : 1;
-  const size_t sm = select_smem_bytes();
-  if (C == 1) k_select<1><<<nseg, nt, sm, st>>>(x, d_in, k, chunk, idx, xs, sel, g_trace);
-  else if (C == 2) k_select<2><<<nseg, nt, sm, st>>>(x, d_in, k, chunk, idx, xs, sel, g_trace);
-  else k_select<4><<<nseg, nt, sm, st>>>(x, d_in, k, chunk, idx, xs, sel, g_trace);
+  int nt = (n / 8 + 31) / 32 * 32;
+  if (nt > 1024) nt = 1024;
+  k_select<<<nseg, nt, select_block_smem_bytes(n), st>>>(x, d_in, k, chunk, idx, xs, sel);
   return cuda_status(cudaGetLastError());
 }
 
@@ -319,7 +316,10 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
   if (k_sel < 0) return DECDEC_EINVAL;
   if ((s = ensure_attrs()) != DECDEC_OK) return s;
   Prepared P{};
-  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &P.pl)) != DECDEC_OK) return s;
+  const int sel_ctas = k_sel > 0 ? (chunk ? (L->d_in + chunk - 1) / chunk : 1) : 0;
+  const int sel_len = chunk ? (chunk < L->d_in ? chunk : L->d_in) : L->d_in;
+  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &P.pl, sel_ctas > 0 ? sel_ctas : 1, sel_len)) != DECDEC_OK)
+    return s;
   P.p = base_params(L, x, y, P.pl);
   P.k = k;
   P.chunk = chunk;
@@ -344,8 +344,14 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
     p.part = reinterpret_cast<float*>(base + wl.part);
     p.sdev = reinterpret_cast<uint16_t*>(base + wl.sdev);
     p.cnt = reinterpret_cast<uint32_t*>(base + wl.cnt);
+    p.sel_ready = p.cnt + (kCntSlots - kCtrlSlots);
+    p.cta_done = p.sel_ready + 1;
+    p.sel_ctas = sel_ctas;
+    p.k_req = k;
+    p.chunk = chunk;
+    p.sel_out = sel;
     p.n_seg = (L->d_out + kSegCols - 1) / kSegCols;
-    if (p.n_seg > kCntSlots) return DECDEC_EUNSUPPORTED;
+    if (2 * p.n_seg > kCntSlots - kCtrlSlots) return DECDEC_EUNSUPPORTED;
     p.n_rb = (k_sel + kRB - 1) / kRB;
     const int ngw = P.pl.NGW * P.pl.grid;
     int gws = ngw / p.n_seg;
@@ -357,12 +363,10 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
   return DECDEC_OK;
 }
 
-decdec_status enqueue_linear(const Prepared& P, cudaStream_t st) {
-  if (P.p.k_sel == 0) return launch_linear(P.p, P.pl, P.bits, 4, false, st);
-  decdec_status s = launch_select(P.x, P.p.d_in, P.k, P.chunk, const_cast<int*>(P.p.idx),
-                                  const_cast<uint16_t*>(P.p.xs), P.sel, st);
-  if (s != DECDEC_OK) return s;
-  return launch_linear(P.p, P.pl, P.bits, P.rbits, true, st);
+decdec_status enqueue_linear(const Prepared& P, cudaStream_t st, bool chained = false) {
+  Plan pl = P.pl;
+  pl.grid += P.p.sel_ctas;  // selector CTAs first
+  return launch_linear(P.p, pl, P.bits, P.p.k_sel ? P.rbits : 4, chained, st);
 }
 
 }  // namespace
@@ -393,7 +397,7 @@ decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, 
   int n_kernels = 0;
   for (int i = 0; i < n_layers && s == DECDEC_OK; ++i) {
     s = prepare_linear(&layers[i], x[i], k[i], chunk, y[i], nullptr, ws, ws_bytes, &P[i]);
-    n_kernels += P[i].p.k_sel > 0 ? 2 : 1;
+    n_kernels += 1;
   }
   if (s != DECDEC_OK) {
     delete[] P;
@@ -408,7 +412,7 @@ decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, 
   }
   decdec_stack* g = new decdec_stack();
   cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
-  for (int i = 0; i < n_layers && e == cudaSuccess && s == DECDEC_OK; ++i) s = enqueue_linear(P[i], st);
+  for (int i = 0; i < n_layers && e == cudaSuccess && s == DECDEC_OK; ++i) s = enqueue_linear(P[i], st, i > 0);
   cudaGraph_t graph = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(st, &graph);
   cudaStreamDestroy(st);
@@ -466,7 +470,10 @@ decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, si
   return DECDEC_OK;
 }
 
-int32_t decdec_launches_per_call(int32_t k) { return k > 0 ? 2 : 1; }
+int32_t decdec_launches_per_call(int32_t k) {
+  (void)k;
+  return 1;  // selector CTAs, GEMV and gather run in one kernel
+}
 
 decdec_status decdec_debug_trace(void* buf, size_t bytes) {
   if (buf && bytes < (size_t)(2 + 1024 * kTraceEvents) * 8) return DECDEC_ESPACE;

@@ -18,16 +18,18 @@
 //                       R_hat[S, segment] from pinned host memory with zero-copy loads
 //                       (P:251), double-buffered (16 rows in flight per warp), decode + FHFMA,
 //                       one fp32 partial per item.
-// Combine (P:207 step 4; the paper uses atomics): every producer of a 256-column
-// segment (GEMV rows, gather row blocks) publishes with a fence and bumps the segment's
-// arrival counter; the last arriver sums  y = fp16(o_b + S_j * sum_rb part_rb)  in a fixed
-// order and resets the counter.  No value atomics -> bit-reproducible.
+// Combine (P:207 step 4; the paper uses atomics): GEMV warps publish their o_b rows
+// and gather warps their partials, each with one fence and an arrival count per 256-column
+// segment; the segment's last gather warp waits for its o_b rows and writes
+// y = fp16(o_b + S_j * sum_j part_j) in a fixed order, then resets the counters.  No value
+// atomics -> bit-reproducible.
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
 #include <type_traits>
 #include "ptx.cuh"
 #include "decode.cuh"
+#include "select.cuh"
 
 namespace decdec {
 
@@ -36,6 +38,7 @@ constexpr int kSegCols = 256;     // output columns per combine segment (128 B o
 constexpr int kMaxThreads = 480;  // 1 producer + <= 12 consumer + 2 gather warps
 constexpr int kMaxRPS = 4;       // rows per slot per tile
 constexpr int kCntSlots = 4096;   // arrival counters at the head of the workspace
+constexpr int kCtrlSlots = 16;    // last slots of that region: control words (sel_ready, cta_done)
 // trace events (per CTA): 0 start, 1 first TMA issued, 2 x loaded, 3 first stage landed,
 // 4 GEMV done, 5 selector visible, 6 selection staged, 7 gather done, 8 consumer exit
 constexpr int kTraceEvents = 9;
@@ -70,6 +73,13 @@ struct LinearParams {
   int n_seg, n_rb, gws, NGW;  // gws = gather warps per segment (each takes row blocks j, j+gws, ...)
   uint32_t off_sel;            // smem offset of the staged selection (idx int32[k], xs u16[k])
   unsigned long long* trace;   // optional per-CTA event timestamps [grid][kTraceEvents] (ns), or null
+  // step (1) runs on the first sel_ctas CTAs (one per selection segment: the whole x, or one
+  // chunk); each bumps *sel_ready when its indices are written; gather warps wait for
+  // *sel_ready == sel_ctas.  The last CTA to exit resets *sel_ready and *cta_done.
+  int sel_ctas, k_req, chunk;
+  int* sel_out;
+  uint32_t* sel_ready;
+  uint32_t* cta_done;
 };
 
 template <int RBITS>
@@ -105,19 +115,48 @@ __device__ __forceinline__ void combine_segment(const LinearParams& p, int seg, 
   *reinterpret_cast<uint4*>(p.y + col0) = make_uint4(out[0], out[1], out[2], out[3]);
 }
 
-// Publish `add` arrivals for segment `seg`; the warp whose arrival completes the segment
-// combines it.  Caller: all lanes have stored their data and executed __threadfence().
+// GEMV side: publish `rows` o_b rows of segment `seg` (caller fenced its stores).
+__device__ __forceinline__ void gemv_publish(const LinearParams& p, int seg, uint32_t rows, int lane) {
+  __syncwarp();
+  if (lane == 0) atomicAdd(p.cnt + seg, rows);
+}
+
+// Gather side: publish one partial of segment `seg` (caller fenced).  The last of the
+// segment's gws gather warps waits for the segment's o_b rows, combines, and resets both
+// counters for the next call.  Combines are thus spread over the gather warps (one per
+// segment) and never run on the GEMV warps.
 template <int RBITS>
-__device__ __forceinline__ void arrive_segment(const LinearParams& p, int seg, uint32_t add, int lane) {
+__device__ __forceinline__ void gather_publish(const LinearParams& p, int seg, int lane) {
   __syncwarp();
   uint32_t old = 0;
-  if (lane == 0) old = atomicAdd(p.cnt + seg, add);
+  if (lane == 0) old = atomicAdd(p.cnt + p.n_seg + seg, 1u);
   old = __shfl_sync(0xffffffffu, old, 0);
-  const int seg_cols = min(kSegCols, p.d_out - seg * kSegCols);
-  if (old + add == (uint32_t)(seg_cols + p.gws)) {
-    __threadfence();
-    combine_segment<RBITS>(p, seg, lane);
-    if (lane == 0) p.cnt[seg] = 0;  // ready for the next call
+  if (old + 1 != (uint32_t)p.gws) return;
+  const uint32_t seg_cols = (uint32_t)min(kSegCols, p.d_out - seg * kSegCols);
+  if (lane == 0) {
+    while (ld_acquire_gpu(p.cnt + seg) != seg_cols) __nanosleep(32);
+  }
+  __syncwarp();
+  __threadfence();
+  combine_segment<RBITS>(p, seg, lane);
+  if (lane == 0) {
+    p.cnt[seg] = 0;  // ready for the next call
+    p.cnt[p.n_seg + seg] = 0;
+  }
+}
+
+// Called by every warp when it is done (all lanes).  With compensation (k_sel > 0) the last
+// warp of the last CTA resets the PDL-chain control words for the next layer.
+__device__ __forceinline__ void warp_exit(const LinearParams& p, uint32_t* warps_done, int lane) {
+  if (p.k_sel <= 0) return;
+  __syncwarp();
+  if (lane == 0) {
+    if (atomicAdd(warps_done, 1u) == (blockDim.x >> 5) - 1) {       // last warp of this CTA
+      if (atomicAdd(p.cta_done, 1u) == gridDim.x - 1) {               // last CTA of the grid
+        *p.cta_done = 0u;
+        *p.sel_ready = 0u;
+      }
+    }
   }
 }
 
@@ -129,8 +168,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
   uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * p.NSLOTS * 4 * max(p.NKW, 1));
   uint64_t* empty = full + p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ uint32_t warps_done;
+  // Let the next kernel of the stream launch now: its CTAs take SMs as ours retire and start
+  // streaming their (static) weights while we finish (cross-layer overlap).
+  pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
+    warps_done = 0;
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], p.NC);
@@ -140,13 +184,36 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
   __syncthreads();
   if (threadIdx.x == 0) DECDEC_TRACE(p, 0);
 
+  // ------------------------------------------------------------------ selector CTAs (step 1)
+  if ((int)blockIdx.x < p.sel_ctas) {
+    pdl_wait();  // x may be the previous layer's product
+    if (threadIdx.x == 0) DECDEC_TRACE(p, 5);
+    const int seg = blockIdx.x;
+    const int a = p.chunk ? seg * p.chunk : 0;
+    const int n = p.chunk ? min(p.chunk, p.d_in - a) : p.d_in;
+    const int q = p.chunk ? min(p.k_req, n) : p.k_req;
+    const int off = p.chunk ? seg * p.k_req : 0;
+    select_block(p.x + a, n, q, a, const_cast<int*>(p.idx) + off, const_cast<uint16_t*>(p.xs) + off,
+                 p.sel_out ? p.sel_out + off : nullptr, reinterpret_cast<SelectSmem*>(smem),
+                 reinterpret_cast<uint4*>(smem + sizeof(SelectSmem)));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(p.sel_ready, 1u);
+      DECDEC_TRACE(p, 6);
+    }
+    warp_exit(p, &warps_done, lane);
+    return;
+  }
+  const int cta = blockIdx.x - p.sel_ctas, n_cta = gridDim.x - p.sel_ctas;  // GEMV CTA index / count
+
   // ------------------------------------------------------------------ producer (TMA)
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       const uint32_t wb = (uint32_t)p.TR * p.row_bytes, sb = (uint32_t)p.TR * p.G * 2, zb = (uint32_t)p.TR * p.G;
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+      for (int tile = cta; tile < p.n_tiles; tile += n_cta, ++it) {
         const int st = it % p.stages;
         if (it >= p.stages) mbar_wait(&empty[st], ((it / p.stages) & 1) ^ 1);
         uint8_t* dst = stage0 + (size_t)st * p.stage_bytes;
@@ -157,6 +224,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
         if (it == 0) DECDEC_TRACE(p, 1);
       }
     }
+    warp_exit(p, &warps_done, lane);
     return;
   }
 
@@ -171,6 +239,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     const int slot = small_g ? (cw * (32 / G) + lane / G) : (cw / max(p.NKW, 1));
     const bool active = g < G;
     const int rot = (BITS == 4) ? ((g >> 1) & 3) : 0;  // 4-bit: bank-conflict-free 16-B chunk order
+    // x (and the workspace) belong to the previous layer until it completes
+    pdl_wait();
     uint32_t xr[64];
     float Xs = 0.f;
     if (active) {
@@ -205,7 +275,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     const int team = cw / nkw, wi = cw % nkw;
     int nrows_tile = 0;  // o_b rows this warp writes per tile (same for every tile)
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+    for (int tile = cta; tile < p.n_tiles; tile += n_cta, ++it) {
       const int st = it % p.stages;
       mbar_wait(&full[st], (it / p.stages) & 1);
       if (it == 0 && ct == 0) DECDEC_TRACE(p, 3);
@@ -341,26 +411,30 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     // a fence per tile stalled the GEMV stream by ~1 µs each.
     if (p.k_sel > 0 && nrows_tile > 0) {
       __threadfence();
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x)
-        arrive_segment<RBITS>(p, (tile * p.TR) / kSegCols, (uint32_t)nrows_tile, lane);
+      for (int tile = cta; tile < p.n_tiles; tile += n_cta)
+        gemv_publish(p, (tile * p.TR) / kSegCols, (uint32_t)nrows_tile, lane);
     }
+    warp_exit(p, &warps_done, lane);
     return;
   }
 
   // ------------------------------------------------------------------ gather warps (DEC)
-  if (p.k_sel <= 0) return;
+  if (p.k_sel <= 0) return;  // (no gather warps are launched without compensation)
   const int gwi = warp - 1 - p.NC;
   int* sidx = reinterpret_cast<int*>(smem + p.off_sel);
   uint16_t* sxs = reinterpret_cast<uint16_t*>(sidx + p.k_sel);
-  pdl_wait();  // selector kernel complete and its writes visible
-  if (gwi == 0 && lane == 0) DECDEC_TRACE(p, 5);
+  pdl_wait();  // the workspace belongs to the previous layer until it completes
+  if (lane == 0) {
+    while (ld_acquire_gpu(p.sel_ready) < (uint32_t)p.sel_ctas) __nanosleep(20);
+  }
+  __syncwarp();
   for (int i = gwi * 32 + lane; i < p.k_sel; i += p.NGW * 32) {
     sidx[i] = __ldcg(p.idx + i);
     sxs[i] = __ldcg(p.xs + i);
   }
   named_bar_sync(15, p.NGW * 32);
   if (gwi == 0 && lane == 0) DECDEC_TRACE(p, 6);
-  const int gw = gwi + p.NGW * blockIdx.x, ngw = p.NGW * gridDim.x;
+  const int gw = gwi + p.NGW * cta, ngw = p.NGW * n_cta;
   for (int pair = gw; pair < p.n_seg * p.gws; pair += ngw) {
     const int seg = pair % p.n_seg, j = pair / p.n_seg;
     const int col0 = seg * kSegCols + lane * 8;
@@ -428,7 +502,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
   }
   if (gwi == 0 && lane == 0) DECDEC_TRACE(p, 7);
   __threadfence();  // one fence for all of this warp's partials, then the arrivals
-  for (int pair = gw; pair < p.n_seg * p.gws; pair += ngw) arrive_segment<RBITS>(p, pair % p.n_seg, 1u, lane);
+  for (int pair = gw; pair < p.n_seg * p.gws; pair += ngw) gather_publish<RBITS>(p, pair % p.n_seg, lane);
+  warp_exit(p, &warps_done, lane);
 }
 
 // Debug: decode packed weights with the kernel's own decode path; q_out u8 [d_out][d_in].

@@ -103,6 +103,16 @@ __device__ __forceinline__ uint4 ld_zc_u4(const void* p) {
   return v;
 }
 
+// ---------------------------------------------------------------- cross-CTA flags
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ---------------------------------------------------------------- tracing (debug timelines)
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;

@@ -1,18 +1,20 @@
 // Step (1) of DecDEC: exact Top-k of |x| ("Exact").
 //
 // Replaces the paper's 32-bucket approximate, randomly-filled chunk Top-K with
-// an exact, deterministic selection on the 15-bit magnitude key bits(x) & 0x7FFF (ledger L2).
-// One CTA per segment (the whole x for chunk = 0, one chunk otherwise):
-//   1. every thread holds R = 8C contiguous elements in registers; one smem atomicAdd per
-//      element into a 256-bin histogram of key >> 7 (measured ~4 SMSP cycles per warp-op;
-//      activation exponents spread the bins, so lanes rarely collide);
-//   2. one warp finds the bin holding the q-th largest key (lane l owns 8 contiguous bins,
-//      suffix scan over lanes), then a 128-bin histogram of key & 127 over that bin's
-//      elements gives the exact threshold T, `above` = #keys > T, need = q - above ties;
-//   3. per-thread counts of key > T / key == T, one block exclusive scan in index order,
-//      then each thread writes its selected indices (ties: lowest index first).
-// Output ascending by index.  No per-element warp collectives (ballots cost ~8 SMSP
-// cycles each on B200) and a handful of barriers.
+// an exact, deterministic selection on the 15-bit magnitude key bits(x) & 0x7FFF (ledger L2),
+// done by ONE thread block (any size, multiple of 32) over one segment -- the whole x
+// (chunk = 0) or one chunk.  In the fused layer kernel it is CTA 0's job; the
+// standalone decdec_select runs it in its own kernel.
+//   1. x is staged in smem; thread t owns chunks of 8 contiguous elements [tC, tC + C);
+//   2. one smem atomicAdd per element into a 256-bin histogram of key >> 7 (measured ~4
+//      SMSP cycles per warp-op on B200, activation exponents spread the bins); warp 0 finds
+//      the bin holding the q-th largest key (lane l owns 8 contiguous bins, suffix scan over
+//      lanes); a 128-bin histogram of key & 127 over that bin's elements then gives the exact
+//      threshold T, `above` = #keys > T, need = q - above ties to take;
+//   3. per-thread counts of key > T / key == T, one block exclusive scan in index order, and
+//      each thread writes its selected indices (ties: lowest index first), ascending.
+// Warp ballots / reductions cost ~8 SMSP cycles each on B200, so the per-element work avoids
+// them; histogram rows are padded (stride 9 / 5 words) so warp 0's bin reads are conflict-free.
 #pragma once
 #include <cstdint>
 #include "ptx.cuh"
@@ -20,10 +22,17 @@
 namespace decdec {
 
 constexpr int kSelMaxWarps = 32;
-constexpr int kSelMaxThreads = 1024;
 
-// Exclusive scan of v over the block in thread order (warp shuffles + one warp over the warp
-// totals).  `tmp` holds >= 32 words.  Two barriers.
+// shared scratch of select_block (plus the staged x: 2 * roundup(len, 8) bytes after it)
+struct SelectSmem {
+  uint32_t histA[256 + 32];  // bin b at b + (b >> 3)
+  uint32_t histB[128 + 32];  // bin b at b + (b >> 2)
+  uint32_t tmp[kSelMaxWarps];
+  uint32_t bA, aboveA, T, need;
+};
+inline size_t select_block_smem_bytes(int len) { return sizeof(SelectSmem) + (size_t)((len + 7) / 8) * 16; }
+
+// Exclusive scan of v over the block in thread order.  Two barriers.
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* tmp) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   uint32_t inc = v;
@@ -48,175 +57,161 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
   return tmp[wid] + inc - v;
 }
 
-// grid = number of segments; blockDim = NT (multiple of 32, <= 1024) with NT * 8C >= len;
-// dynamic smem = select_smem_bytes().
-template <int C>
-__global__ void __launch_bounds__(kSelMaxThreads) k_select(const uint16_t* __restrict__ x, int d_in, int k, int chunk,
-                                                           int* __restrict__ idx_out, uint16_t* __restrict__ xs_out,
-                                                           int* __restrict__ sel_out, unsigned long long* trace) {
-  constexpr int R = 8 * C;
-  if (trace && threadIdx.x == 0 && blockIdx.x == 0) {
-    trace[0] = globaltimer();
-    trace[2 + 1024 * 9 - 2] = clock64();
+// warp-level: lane l holds counts c[0..PER) of bins [PER*l, PER*l + PER); find the bin that
+// contains the q-th largest key (scanning from the top).  Exactly one lane writes (*bin, *above).
+template <int PER>
+__device__ __forceinline__ void warp_find_bin(const uint32_t* c, uint32_t q, uint32_t* bin, uint32_t* above_out) {
+  const int lane = threadIdx.x & 31;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) sum += c[j];
+  const uint32_t sr = __shfl_sync(0xffffffffu, sum, 31 - lane);
+  uint32_t inc = sr;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
   }
-  // Programmatic dependent launch: the fused layer kernel that follows may start its HBM
-  // weight stream now; only its gather warps wait (griddepcontrol.wait) for our results.
-  pdl_launch_dependents();
-  __shared__ uint32_t histA[256];
-  __shared__ uint32_t histB[128];
-  __shared__ uint32_t tmp[kSelMaxWarps];
-  __shared__ uint32_t s_bA, s_aboveA, s_T, s_need;
+  const uint32_t above = __shfl_sync(0xffffffffu, inc, 31 - lane) - sum;  // keys in lanes > l
+  if (above < q && above + sum >= q) {
+    uint32_t run = above;
+#pragma unroll
+    for (int j = PER - 1; j >= 0; --j) {
+      if (run + c[j] >= q) {
+        *bin = (uint32_t)(PER * lane + j);
+        *above_out = run;
+        break;
+      }
+      run += c[j];
+    }
+  }
+}
+
+// 16-bit element j (0..7) of a 16-B chunk
+__device__ __forceinline__ uint32_t chunk_elem(const uint4& v, int j) {
+  const uint32_t w = (j < 2) ? v.x : (j < 4) ? v.y : (j < 6) ? v.z : v.w;
+  return (j & 1) ? (w >> 16) : (w & 0xffffu);
+}
+
+// Exact top-q of the n keys of x (global, 16-B aligned, n % 8 == 0) by the whole block.
+// Writes idx_out[pos] = idx_base + i and xs_out[pos] = x[i] for the selected i in ascending
+// order (pos = 0 .. q-1), and sel_out likewise if non-null.  Ends with a barrier-free tail:
+// callers that consume the outputs in the same block must __syncthreads() (and fence for other
+// blocks).
+__device__ __forceinline__ void select_block(const uint16_t* __restrict__ x, int n, int q, int idx_base,
+                                             int* __restrict__ idx_out, uint16_t* __restrict__ xs_out,
+                                             int* __restrict__ sel_out, SelectSmem* S, uint4* sx4) {
+  const int t = threadIdx.x, NT = blockDim.x, lane = t & 31;
+  const int n8 = n >> 3;
+  const int C = (n8 + NT - 1) / NT;  // chunks of 8 per thread
+  // stage x (coalesced 16-B loads) and zero the histograms
+#pragma unroll 4
+  for (int i = t; i < n8; i += NT) sx4[i] = __ldg(reinterpret_cast<const uint4*>(x) + i);
+  for (int i = t; i < 256 + 32; i += NT) S->histA[i] = 0;
+  for (int i = t; i < 128 + 32; i += NT) S->histB[i] = 0;
+  __syncthreads();
+  const int c0 = t * C, c1 = min(c0 + C, n8);
+  // ---- coarse histogram (key >> 7)
+#pragma unroll 1
+  for (int c = c0; c < c1; ++c) {
+    const uint4 v = sx4[c];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t b = (chunk_elem(v, j) & 0x7fffu) >> 7;
+      atomicAdd(&S->histA[b + (b >> 3)], 1u);
+    }
+  }
+  __syncthreads();
+  if (t < 32) {
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = S->histA[9 * lane + j];
+    warp_find_bin<8>(c, (uint32_t)q, &S->bA, &S->aboveA);
+  }
+  __syncthreads();
+  const uint32_t bA = S->bA, qB = (uint32_t)q - S->aboveA;
+  // ---- fine histogram (key & 127) of bin bA
+#pragma unroll 1
+  for (int c = c0; c < c1; ++c) {
+    const uint4 v = sx4[c];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t key = chunk_elem(v, j) & 0x7fffu;
+      if ((key >> 7) == bA) {
+        const uint32_t b = key & 127u;
+        atomicAdd(&S->histB[b + (b >> 2)], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  if (t < 32) {
+    uint32_t c[4], bin = 0, above = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[j] = S->histB[5 * lane + j];
+    bin = 0xffffffffu;
+    warp_find_bin<4>(c, qB, &bin, &above);
+    if (bin != 0xffffffffu) {
+      S->T = (bA << 7) | bin;
+      S->need = qB - above;
+    }
+  }
+  __syncthreads();
+  const uint32_t T = S->T;
+  const int need = (int)S->need;  // ties (key == T) to take, lowest index first
+  // ---- counts, block scan in index order, placement
+  uint32_t n_gt = 0, n_eq = 0;
+#pragma unroll 1
+  for (int c = c0; c < c1; ++c) {
+    const uint4 v = sx4[c];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t key = chunk_elem(v, j) & 0x7fffu;
+      n_gt += key > T;
+      n_eq += key == T;
+    }
+  }
+  const uint32_t pre = block_exclusive_scan((n_eq << 16) | n_gt, S->tmp);
+  if (n_gt + n_eq) {
+    int eq_seen = (int)(pre >> 16);
+    int pos = (int)(pre & 0xffffu) + min(eq_seen, need);
+#pragma unroll 1
+    for (int c = c0; c < c1; ++c) {
+      const uint4 v = sx4[c];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t raw = chunk_elem(v, j);
+        const uint32_t key = raw & 0x7fffu;
+        bool take = key > T;
+        if (key == T) {
+          take = eq_seen < need;
+          ++eq_seen;
+        }
+        if (take) {
+          const int i = idx_base + 8 * c + j;
+          idx_out[pos] = i;
+          xs_out[pos] = (uint16_t)raw;
+          if (sel_out) sel_out[pos] = i;
+          ++pos;
+        }
+      }
+    }
+  }
+  (void)lane;
+}
+
+// Standalone selector (decdec_select): one block per segment.
+__global__ void __launch_bounds__(1024) k_select(const uint16_t* __restrict__ x, int d_in, int k, int chunk,
+                                                 int* __restrict__ idx_out, uint16_t* __restrict__ xs_out,
+                                                 int* __restrict__ sel_out) {
+  extern __shared__ __align__(16) uint8_t dsm[];
   const int seg = blockIdx.x;
   const int a = chunk ? seg * chunk : 0;
   const int n = chunk ? min(chunk, d_in - a) : d_in;
   const int q = chunk ? min(k, n) : k;
   const int out_off = chunk ? seg * k : 0;  // every earlier chunk is full length >= k
   if (q <= 0) return;
-  const int t = threadIdx.x, NT = blockDim.x, lane = t & 31;
-#define SEL_PHASE(i) \
-  if (trace && t == 0 && blockIdx.x == 0) trace[2 + 1024 * 9 - 16 + (i)] = clock64();
-
-  // R contiguous elements per thread (16-B loads in flight while the histograms are zeroed)
-  const int base = t * R;
-  uint32_t raw[R / 2];
-#pragma unroll
-  for (int v = 0; v < C; ++v) {
-    uint4 q4 = make_uint4(0, 0, 0, 0);
-    if (base + 8 * v < n) q4 = __ldg(reinterpret_cast<const uint4*>(x + a + base) + v);
-    raw[4 * v + 0] = q4.x; raw[4 * v + 1] = q4.y; raw[4 * v + 2] = q4.z; raw[4 * v + 3] = q4.w;
-  }
-  const int nv = n - base;  // slot e < nv is a real element
-  auto key_of = [&](int e) -> uint32_t { return ((e & 1) ? (raw[e >> 1] >> 16) : raw[e >> 1]) & 0x7fffu; };
-  for (int i = t; i < 256; i += NT) histA[i] = 0;
-  for (int i = t; i < 128; i += NT) histB[i] = 0;
-  __syncthreads();
-  SEL_PHASE(0);
-
-  // ---- 1. coarse histogram (key >> 7)
-#pragma unroll
-  for (int e = 0; e < R; ++e)
-    if (e < nv) atomicAdd(&histA[key_of(e) >> 7], 1u);
-  __syncthreads();
-  SEL_PHASE(1);
-  // ---- 2a. warp 0: bin of the q-th largest key; lane l owns bins [8l, 8l + 8)
-  if (t < 32) {
-    uint32_t c[8], sum = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      c[j] = histA[8 * lane + j];
-      sum += c[j];
-    }
-    // keys above lane l's bins = sum over lanes > l: inclusive scan over reversed lanes
-    const uint32_t sr = __shfl_sync(0xffffffffu, sum, 31 - lane);
-    uint32_t inc = sr;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
-    }
-    // inc at reversed position r = 31 - l is sum over lanes >= l; above_l = that - sum_l
-    const uint32_t above = __shfl_sync(0xffffffffu, inc, 31 - lane) - sum;
-    if (above < (uint32_t)q && above + sum >= (uint32_t)q) {
-      uint32_t run = above;
-#pragma unroll
-      for (int j = 7; j >= 0; --j) {
-        if (run + c[j] >= (uint32_t)q) {
-          s_bA = 8 * lane + j;
-          s_aboveA = run;
-          break;
-        }
-        run += c[j];
-      }
-    }
-  }
-  __syncthreads();
-  const uint32_t bA = s_bA, aboveA = s_aboveA;
-  // ---- 2b. fine histogram (key & 127) of the elements in bin bA
-#pragma unroll
-  for (int e = 0; e < R; ++e) {
-    const uint32_t key = key_of(e);
-    if (e < nv && (key >> 7) == bA) atomicAdd(&histB[key & 127u], 1u);
-  }
-  __syncthreads();
-  if (t < 32) {  // lane l owns fine bins [4l, 4l + 4)
-    uint32_t c[4], sum = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      c[j] = histB[4 * lane + j];
-      sum += c[j];
-    }
-    const uint32_t sr = __shfl_sync(0xffffffffu, sum, 31 - lane);
-    uint32_t inc = sr;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
-    }
-    const uint32_t qq = (uint32_t)q - aboveA;
-    const uint32_t above = __shfl_sync(0xffffffffu, inc, 31 - lane) - sum;
-    if (above < qq && above + sum >= qq) {
-      uint32_t run = above;
-#pragma unroll
-      for (int j = 3; j >= 0; --j) {
-        if (run + c[j] >= qq) {
-          s_T = (bA << 7) | (uint32_t)(4 * lane + j);
-          s_need = qq - run;
-          break;
-        }
-        run += c[j];
-      }
-    }
-  }
-  __syncthreads();
-  const uint32_t T = s_T;
-  const int need = (int)s_need;  // ties (key == T) to take, lowest index first
-  SEL_PHASE(2);
-
-  // ---- 3. per-thread counts, block exclusive scan of packed (eq << 16 | gt) in index order
-  uint32_t n_gt = 0, n_eq = 0;
-#pragma unroll
-  for (int e = 0; e < R; ++e) {
-    const uint32_t key = key_of(e);
-    n_gt += e < nv && key > T;
-    n_eq += e < nv && key == T;
-  }
-  const uint32_t v = (n_eq << 16) | n_gt;
-  const uint32_t pre = block_exclusive_scan(v, tmp);
-  SEL_PHASE(3);
-  if (n_gt + n_eq) {
-    int eq_seen = (int)(pre >> 16);
-    int pos = (int)(pre & 0xffffu) + min(eq_seen, need);
-#pragma unroll
-    for (int e = 0; e < R; ++e) {
-      const uint32_t key = key_of(e);
-      bool take = e < nv && key > T;
-      if (e < nv && key == T) {
-        take = eq_seen < need;
-        ++eq_seen;
-      }
-      if (take) {
-        const uint32_t h = (e & 1) ? (raw[e >> 1] >> 16) : (raw[e >> 1] & 0xffffu);
-        idx_out[out_off + pos] = a + base + e;
-        xs_out[out_off + pos] = (uint16_t)h;
-        if (sel_out) sel_out[out_off + pos] = a + base + e;
-        ++pos;
-      }
-    }
-  }
-  if (trace && t == 0 && blockIdx.x == 0) {
-    trace[1] = globaltimer();
-    trace[2 + 1024 * 9 - 1] = clock64();
-  }
-#undef SEL_PHASE
+  select_block(x + a, n, q, a, idx_out + out_off, xs_out + out_off, sel_out ? sel_out + out_off : nullptr,
+               reinterpret_cast<SelectSmem*>(dsm), reinterpret_cast<uint4*>(dsm + sizeof(SelectSmem)));
 }
-
-// launch geometry for a segment of len elements: NT threads of C 8-element chunks
-inline void select_geometry(int len, int* nt, int* C) {
-  int c = 1;
-  while (c < 4 && (len + 8 * c - 1) / (8 * c) > kSelMaxThreads) c *= 2;
-  *nt = ((len + 8 * c - 1) / (8 * c) + 31) / 32 * 32;
-  *C = c;
-}
-inline size_t select_smem_bytes() { return 0; }
 
 }  // namespace decdec

@@ -49,14 +49,14 @@ for rep in range(2):
 dd.decdec_debug_trace(0, 0)
 import json  # noqa: E402
 plan = json.loads(lins[0].plan(k))
-grid = plan["grid"]
+grid = plan["grid"] + (1 if k else 0)  # + selector CTA
 print("plan", plan)
 prev_end = None
 for i in range(a.n):
     t = bufs[i].cpu().numpy()
-    sel0, sel1 = t[0], t[1]
     ev = t[2: 2 + grid * 9].reshape(grid, 9).astype(np.float64)
-    base = sel0 if k else ev[:, 0][ev[:, 0] > 0].min()
+    base = ev[:, 0][ev[:, 0] > 0].min()
+    sel0, sel1 = (ev[0, 5], ev[0, 6]) if k else (0, 0)
     rel = (ev - base) / 1e3
     line = [f"call {i}"]
     if k:
