@@ -164,7 +164,9 @@ decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out,
 /* Debug timelines: while buf != NULL every launch records %globaltimer (ns) events into buf
  * (u64: [0..1] unused, then per CTA 9 events: start, first bulk copy issued, x loaded, first
  * stage landed, GEMV done, selector start / selection staged, selection published, gather
- * done; selector CTAs come first).  bytes >= (2 + 1024*9)*8.  Not thread-safe; NULL disables. */
+ * done; selector CTAs come first).  bytes >= (2 + 1024*9)*8.  Stacks created while tracing give
+ * layer i the region starting at u64 2 + i*160*9 (bytes >= (2 + n_layers*1440)*8).  Not
+ * thread-safe; NULL disables. */
 decdec_status decdec_debug_trace(void* buf, size_t bytes);
 
 /* Launch plan chosen for a layer (tile rows, consumer warps, stages, grid) as text. */

@@ -38,7 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     cmd = [
         nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-        "-cudart", "shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+        "-cudart", "shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC, *os.environ.get("DECDEC_NVCC_EXTRA", "").split(),
         "-Xptxas", "-v" if verbose else "-O3",
         "-o", LIB + ".tmp", *sources(),
     ]

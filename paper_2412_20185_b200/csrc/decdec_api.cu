@@ -30,6 +30,7 @@ int device_sms() {
 }
 
 unsigned long long* g_trace = nullptr;  // debug timelines (decdec_debug_trace)
+constexpr size_t kTraceStride = 160 * 9;  // u64 per layer in stack traces (<= 160 CTAs)
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -37,7 +38,7 @@ int gcd(int a, int b) { while (b) { int t = a % b; a = b; b = t; } return a; }
 
 struct Plan {
   int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, NGW;
-  uint32_t stage_bytes, off_s, off_z, off_sel;
+  uint32_t stage_bytes, off_s, off_z, off_sel, off_x;
   size_t smem;
 };
 
@@ -80,17 +81,32 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
       p.stage_bytes = (uint32_t)align_up(p.off_z + (uint32_t)p.TR * G, 16);
       const size_t red = (size_t)2 * p.NSLOTS * 4 * (nkw ? nkw : 1) * 4;
       const size_t sel = align_up((size_t)k_sel * 6, 16);
-      const size_t avail = kSmemBudget - red - 16 * 8 - sel;
+      const size_t xb = align_up((size_t)d_in * 2, 16);  // staged x (swizzled, see k_linear)
+      const size_t avail = kSmemBudget - red - 16 * 8 - sel - xb;
       p.stages = (int)(avail / p.stage_bytes);
       if (p.stages > 8) p.stages = 8;
       if (p.stages < 2) continue;
+      // Cap the bytes in flight per SM near what Little's law needs at HBM latency: a deeper
+      // ring does not add bandwidth, it only queues ~µs of traffic ahead of latency-critical
+      // loads (x, selection, gather bookkeeping).
+      {
+        static int env_kb = -1;
+        if (env_kb < 0) {
+          const char* e = getenv("DECDEC_INFLIGHT_KB");
+          env_kb = e ? atoi(e) : 64;
+        }
+        int cap = (int)(((size_t)env_kb * 1024) / p.stage_bytes);
+        if (cap < 2) cap = 2;
+        if (p.stages > cap) p.stages = cap;
+      }
       p.n_tiles = d_out / p.TR;
       // k > 0: the selector CTA(s) take the first SMs; GEMV CTAs fill the rest
       const int max_grid = k_sel > 0 ? sms - sel_ctas : sms;
       p.grid = p.n_tiles < max_grid ? p.n_tiles : max_grid;
       p.NGW = k_sel > 0 ? 2 : 0;
       p.off_sel = (uint32_t)((size_t)p.stages * p.stage_bytes + red + (size_t)2 * p.stages * 8);
-      p.smem = p.off_sel + sel;
+      p.off_x = (uint32_t)align_up((size_t)p.off_sel + sel, 16);
+      p.smem = p.off_x + xb;
       if (k_sel > 0 && p.smem < select_block_smem_bytes(sel_len)) p.smem = select_block_smem_bytes(sel_len);
       const double waves = (double)((p.n_tiles + sms - 1) / sms);
       const double cost = waves * ((double)p.stage_bytes + 3072.0) * (nc < 4 ? 1.0 + 0.15 * (4 - nc) : 1.0);
@@ -246,7 +262,14 @@ LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, 
   p.off_z = pl.off_z;
   p.NGW = pl.NGW;
   p.off_sel = pl.off_sel;
+  p.off_x = pl.off_x;
   p.trace = g_trace ? g_trace + 2 : nullptr;
+  static int env_prefetch = -1;
+  if (env_prefetch < 0) {
+    const char* e = getenv("DECDEC_PREFETCH");
+    env_prefetch = e ? atoi(e) : 1;
+  }
+  p.prefetch = env_prefetch;
   return p;
 }
 
@@ -397,6 +420,8 @@ decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, 
   int n_kernels = 0;
   for (int i = 0; i < n_layers && s == DECDEC_OK; ++i) {
     s = prepare_linear(&layers[i], x[i], k[i], chunk, y[i], nullptr, ws, ws_bytes, &P[i]);
+    // debug timelines: one trace region per layer (decdec_debug_trace buffer must hold them)
+    if (g_trace) P[i].p.trace = g_trace + 2 + (size_t)i * kTraceStride;
     n_kernels += 1;
   }
   if (s != DECDEC_OK) {

@@ -40,7 +40,7 @@ constexpr int kMaxRPS = 4;       // rows per slot per tile
 constexpr int kCntSlots = 4096;   // arrival counters at the head of the workspace
 constexpr int kCtrlSlots = 16;    // last slots of that region: control words (sel_ready, cta_done)
 // trace events (per CTA): 0 start, 1 first TMA issued, 2 x loaded, 3 first stage landed,
-// 4 GEMV done, 5 selector visible, 6 selection staged, 7 gather done, 8 consumer exit
+// 4 GEMV done, 5 selector start, 6 selection published, 7 gather done, 8 consumers released (PDL)
 constexpr int kTraceEvents = 9;
 #define DECDEC_TRACE(p, ev)                                                        \
   do {                                                                             \
@@ -72,11 +72,13 @@ struct LinearParams {
   uint32_t* cnt;
   int n_seg, n_rb, gws, NGW;  // gws = gather warps per segment (each takes row blocks j, j+gws, ...)
   uint32_t off_sel;            // smem offset of the staged selection (idx int32[k], xs u16[k])
+  uint32_t off_x;              // smem offset of the staged x (d_in fp16, 16-B units swizzled)
   unsigned long long* trace;   // optional per-CTA event timestamps [grid][kTraceEvents] (ns), or null
   // step (1) runs on the first sel_ctas CTAs (one per selection segment: the whole x, or one
   // chunk); each bumps *sel_ready when its indices are written; gather warps wait for
   // *sel_ready == sel_ctas.  The last CTA to exit resets *sel_ready and *cta_done.
   int sel_ctas, k_req, chunk;
+  int prefetch;  // weight tiles requested per CTA before griddepcontrol.wait
   int* sel_out;
   uint32_t* sel_ready;
   uint32_t* cta_done;
@@ -212,16 +214,24 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       const uint32_t wb = (uint32_t)p.TR * p.row_bytes, sb = (uint32_t)p.TR * p.G * 2, zb = (uint32_t)p.TR * p.G;
-      int it = 0;
+      const int stages = p.stages;
+      int it = 0, st = 0;
+      uint32_t ph = 0;  // phase of the current pass over the ring
       for (int tile = cta; tile < p.n_tiles; tile += n_cta, ++it) {
-        const int st = it % p.stages;
-        if (it >= p.stages) mbar_wait(&empty[st], ((it / p.stages) & 1) ^ 1);
+        // only `prefetch` tiles may be requested before the previous layer completes: a deeper
+        // early burst floods the memory pipe and delays the x loads the consumers wait on
+        if (it == p.prefetch) pdl_wait();
+        if (it >= stages) mbar_wait(&empty[st], ph ^ 1);
         uint8_t* dst = stage0 + (size_t)st * p.stage_bytes;
         mbar_arrive_expect_tx(&full[st], wb + sb + zb);
         bulk_g2s(dst, p.w + (size_t)tile * wb, wb, &full[st], pol);
         bulk_g2s(dst + p.off_s, p.ws + (size_t)tile * p.TR * p.G, sb, &full[st], pol);
         bulk_g2s(dst + p.off_z, p.wz + (size_t)tile * p.TR * p.G, zb, &full[st], pol);
         if (it == 0) DECDEC_TRACE(p, 1);
+        if (++st == stages) {
+          st = 0;
+          ph ^= 1;
+        }
       }
     }
     warp_exit(p, &warps_done, lane);
@@ -241,27 +251,49 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     const int rot = (BITS == 4) ? ((g >> 1) & 3) : 0;  // 4-bit: bank-conflict-free 16-B chunk order
     // x (and the workspace) belong to the previous layer until it completes
     pdl_wait();
+    if (ct == 0) DECDEC_TRACE(p, 8);
+    // Stage x in smem first: a lane owns 256 contiguous bytes of x, so loading its registers
+    // straight from global memory touches 32 cache lines per instruction and the L1 serialises
+    // them (~5000 cycles for 12 warps, measured).  Coalesced 16-B loads by all consumer threads
+    // -> smem with unit c of group g stored at g*16 + (c ^ (g & 7)) -> conflict-free 16-B reads.
+    uint4* xsm = reinterpret_cast<uint4*>(smem + p.off_x);
+    {
+      const int nx = p.d_in >> 3, nct = p.NC * 32;
+      const uint4* xg = reinterpret_cast<const uint4*>(p.x);
+      for (int u = ct; u < nx; u += nct) {
+        const uint4 v = ld_nc_u4(xg + u);
+        xsm[(u & ~15) | ((u & 15) ^ ((u >> 4) & 7))] = v;
+      }
+      named_bar_sync(14, nct);
+    }
     uint32_t xr[64];
     float Xs = 0.f;
     if (active) {
-      const uint4* xp = reinterpret_cast<const uint4*>(p.x + (size_t)g * 128);
+      const uint4* xp = xsm + g * 16;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int c = (j + rot) & 3;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint4 v = __ldg(xp + 4 * c + e);
+          const uint4 v = xp[(4 * c + e) ^ (g & 7)];
           xr[16 * j + 4 * e + 0] = v.x;
           xr[16 * j + 4 * e + 1] = v.y;
           xr[16 * j + 4 * e + 2] = v.z;
           xr[16 * j + 4 * e + 3] = v.w;
         }
       }
+      if (ct == 0) DECDEC_TRACE(p, 5);
+#ifndef DECDEC_NO_XS
+      // sum of the group's 128 x in fp32: FHFMA with 1.0 into 8 independent accumulators
+      float xa[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      const uint32_t one2 = 0x3C003C00u;  // (1.0, 1.0) as half2
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
-        Xs += __half2float(__ushort_as_half((unsigned short)(xr[i] & 0xffffu)));
-        Xs += __half2float(__ushort_as_half((unsigned short)(xr[i] >> 16)));
+        xa[i & 3] = fhfma_lo(one2, xr[i], xa[i & 3]);
+        xa[4 + (i & 3)] = fhfma_hi(one2, xr[i], xa[4 + (i & 3)]);
       }
+      Xs = ((xa[0] + xa[1]) + (xa[2] + xa[3])) + ((xa[4] + xa[5]) + (xa[6] + xa[7]));
+#endif
       Xs *= 5.9604644775390625e-08f;  // 2^-24: same scale as the decoded codes
     } else {
 #pragma unroll
@@ -274,10 +306,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     const int nkw = small_g ? 1 : p.NKW;
     const int team = cw / nkw, wi = cw % nkw;
     int nrows_tile = 0;  // o_b rows this warp writes per tile (same for every tile)
-    int it = 0;
+    const int stages = p.stages, RPS = p.RPS, NSLOTS = p.NSLOTS, TR = p.TR, row_bytes = p.row_bytes;
+    const int rows_per_warp_tile = small_g ? RPS * (32 / G) : RPS;  // o_b rows one warp (team) writes
+    int it = 0, st = 0;
+    uint32_t ph = 0;
     for (int tile = cta; tile < p.n_tiles; tile += n_cta, ++it) {
-      const int st = it % p.stages;
-      mbar_wait(&full[st], (it / p.stages) & 1);
+      mbar_wait(&full[st], ph);
       if (it == 0 && ct == 0) DECDEC_TRACE(p, 3);
       const uint8_t* sw = stage0 + (size_t)st * p.stage_bytes;
       const uint16_t* ss = reinterpret_cast<const uint16_t*>(sw + p.off_s);
@@ -285,12 +319,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       float part[4] = {0.f, 0.f, 0.f, 0.f};  // RPS <= 4
 #pragma unroll
       for (int m = 0; m < kMaxRPS; m += 2) {
-        if (m >= p.RPS) break;
-        const bool two = m + 1 < p.RPS;
-        const int r0 = slot + m * p.NSLOTS, r1 = slot + (m + 1) * p.NSLOTS;
+        if (m >= RPS) break;
+        const bool two = m + 1 < RPS;
+        const int r0 = slot + m * NSLOTS, r1 = slot + (m + 1) * NSLOTS;
         if (active) {
-          const uint8_t* g0 = sw + (size_t)r0 * p.row_bytes + g * GB;
-          const uint8_t* g1 = sw + (size_t)(two ? r1 : r0) * p.row_bytes + g * GB;
+          const uint8_t* g0 = sw + r0 * row_bytes + g * GB;
+          const uint8_t* g1 = sw + (two ? r1 : r0) * row_bytes + g * GB;
           float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, a1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
           if (BITS == 4) {
             uint4 v0[4], v1[4];
@@ -343,7 +377,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       if (small_g) {
         // rows are whole inside the warp: butterfly over the G lanes of each row (fixed order)
 #pragma unroll
-        if (G == 32 && p.RPS == 4) {
+        if (G == 32 && RPS == 4) {
           // transposed butterfly: 4 rows in 6 shuffles / 5 dependent rounds (fixed order)
           const bool hi16 = lane & 16, hi8 = lane & 8;
           float u0 = (hi16 ? part[2] : part[0]) + __shfl_xor_sync(0xffffffffu, hi16 ? part[0] : part[2], 16);
@@ -353,40 +387,40 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
           for (int o = 4; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
           if ((lane & 7) == 0) {  // lane 0 -> row 0, 8 -> 1, 16 -> 2, 24 -> 3
             const int m = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
-            const int row = tile * p.TR + slot + m * p.NSLOTS;
+            const int row = tile * TR + slot + m * NSLOTS;
             if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
             else p.ob[row] = v;
           }
-        } else if (G == 32 && p.RPS == 2) {
+        } else if (G == 32 && RPS == 2) {
           const bool hi16 = lane & 16;
           float v = (hi16 ? part[1] : part[0]) + __shfl_xor_sync(0xffffffffu, hi16 ? part[0] : part[1], 16);
 #pragma unroll
           for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
           if ((lane & 15) == 0) {
-            const int row = tile * p.TR + slot + (hi16 ? 1 : 0) * p.NSLOTS;
+            const int row = tile * TR + slot + (hi16 ? 1 : 0) * NSLOTS;
             if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
             else p.ob[row] = v;
           }
         } else {
 #pragma unroll
           for (int m = 0; m < kMaxRPS; ++m) {
-            if (m >= p.RPS) break;
+            if (m >= RPS) break;
             float v = part[m];
             for (int o = G >> 1; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if (g == 0) {
-              const int row = tile * p.TR + slot + m * p.NSLOTS;
+              const int row = tile * TR + slot + m * NSLOTS;
               if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
               else p.ob[row] = v;
             }
           }
         }
-        nrows = p.RPS * (32 / G);
+        nrows = rows_per_warp_tile;
       } else {
         // NKW warps per row: warp butterfly, then the team's first warp sums the NKW partials
-        float* rbuf = red + ((it & 1) * p.NSLOTS + team) * 4 * p.NKW;
+        float* rbuf = red + ((it & 1) * NSLOTS + team) * 4 * p.NKW;
 #pragma unroll
         for (int m = 0; m < kMaxRPS; ++m) {
-          if (m >= p.RPS) break;
+          if (m >= RPS) break;
           float v = part[m];
 #pragma unroll
           for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -394,17 +428,21 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
         }
         named_bar_sync(1 + team, p.NKW * 32);
         if (wi == 0) {
-          if (lane < p.RPS) {
+          if (lane < RPS) {
             float v = 0.f;
             for (int w = 0; w < p.NKW; ++w) v += rbuf[lane * p.NKW + w];
-            const int row = tile * p.TR + slot + lane * p.NSLOTS;
+            const int row = tile * TR + slot + lane * NSLOTS;
             if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
             else p.ob[row] = v;
           }
-          nrows = p.RPS;
+          nrows = RPS;
         }
       }
       nrows_tile = nrows;
+      if (++st == stages) {
+        st = 0;
+        ph ^= 1;
+      }
     }
     if (ct == 0) DECDEC_TRACE(p, 4);
     // Publish o_b rows once per warp (one fence for all tiles, then one arrival per tile):
@@ -412,7 +450,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     if (p.k_sel > 0 && nrows_tile > 0) {
       __threadfence();
       for (int tile = cta; tile < p.n_tiles; tile += n_cta)
-        gemv_publish(p, (tile * p.TR) / kSegCols, (uint32_t)nrows_tile, lane);
+        gemv_publish(p, (tile * TR) / kSegCols, (uint32_t)nrows_tile, lane);
     }
     warp_exit(p, &warps_done, lane);
     return;

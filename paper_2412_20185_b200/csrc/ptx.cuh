@@ -89,6 +89,12 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // L2-coherent (bypass L1) loads for data produced by other CTAs in the same launch.
 __device__ __forceinline__ float4 ld_cg_f4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ uint4 ld_cg_u4(const void* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
+// read-only global load, issued in program order relative to other volatile asm
+__device__ __forceinline__ uint4 ld_nc_u4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
 // zero-copy (host mapped) read-only loads, do not allocate in L1
 __device__ __forceinline__ uint32_t ld_zc_u32(const void* p) {
   uint32_t v;
