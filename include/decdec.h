@@ -85,9 +85,10 @@ typedef struct decdec_layer {
   const uint16_t* r_scales;  /* HOST mapped fp16 [d_out] (r_bits = 4) | NULL (r_bits = 16) */
 } decdec_layer;
 
-/* Bytes of workspace for layers with k <= max_k and d_out <= max_d_out: the paper's
- * k x (4+2) B sc_indices/x[sc_indices] buffer plus fp32 partial outputs and
- * per-256-column arrival counters used by the deterministic combine. */
+/* Bytes of workspace for layers with k <= max_k and d_out <= max_d_out: the fp32 base
+ * output o_b (d_out) and per-256-column arrival counters used by the deterministic combine.
+ * (The paper's k x (4+2) B sc_indices / x[sc_indices] buffer lives in the shared
+ * memory of each DEC CTA; max_k no longer changes the size, it is kept for ABI stability.) */
 size_t decdec_workspace_bytes(int32_t max_k, int32_t max_d_out);
 
 /* Zero a workspace (stream-ordered).  Required once before first use. */
@@ -165,7 +166,7 @@ decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out,
  * (u64: [0..1] unused, then per CTA 9 events: start, first bulk copy issued, x loaded, first
  * stage landed, GEMV done, selector start / selection staged, selection published, gather
  * done; selector CTAs come first).  bytes >= (2 + 1024*9)*8.  Stacks created while tracing give
- * layer i the region starting at u64 2 + i*160*9 (bytes >= (2 + n_layers*1440)*8).  Not
+ * layer i the region starting at u64 2 + i*160*20 (bytes >= (2 + n_layers*3200)*8).  Not
  * thread-safe; NULL disables. */
 decdec_status decdec_debug_trace(void* buf, size_t bytes);
 

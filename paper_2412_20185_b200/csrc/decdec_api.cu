@@ -30,15 +30,14 @@ int device_sms() {
 }
 
 unsigned long long* g_trace = nullptr;  // debug timelines (decdec_debug_trace)
-constexpr size_t kTraceStride = 160 * 9;  // u64 per layer in stack traces (<= 160 CTAs)
+constexpr size_t kTraceStride = 160 * 20;  // u64 per layer in stack traces (<= 160 CTAs)
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-int gcd(int a, int b) { while (b) { int t = a % b; a = b; b = t; } return a; }
-
 struct Plan {
-  int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, NGW;
-  uint32_t stage_bytes, off_s, off_z, off_sel, off_x;
+  int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, n_dec;  // grid = GEMV CTAs (+ n_dec DEC CTAs)
+  int n_seg, rpi, gws;  // DEC: output segments, selected rows per gather item, items per segment
+  uint32_t stage_bytes, off_s, off_z, off_sel, off_x, off_part, off_rsc;
   size_t smem;
 };
 
@@ -47,7 +46,56 @@ constexpr size_t kSmemBudget = 200 * 1024;
 // Launch plan: enumerate (consumer warps NC, rows per slot RPS); pick the one minimising the
 // busiest CTA's bytes (ceil(tiles / SMs) x (stage bytes + a per-tile overhead equivalent)),
 // ties -> more consumer warps.  DECDEC_PLAN="NC,RPS" overrides (tuning).
-decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int sel_ctas = 1, int sel_len = 0) {
+// Number of DEC CTAs: enough warps for ~4k zero-copy loads in flight (measured: 128 warps x 32
+// rows saturate PCIe from 4-8 SMs); DECDEC_NDEC overrides.
+int dec_ctas(int warps_per_cta) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DECDEC_NDEC");
+    env = e ? atoi(e) : 0;
+  }
+  if (env > 0) return env;
+  int n = (136 + warps_per_cta - 1) / warps_per_cta;
+  return n < 2 ? 2 : (n > 16 ? 16 : n);
+}
+
+// DEC CTA layout: CTA c owns segments c, c + n_dec, ...; a segment's k_sel rows are split in
+// gws items of rpi rows, sized so that every warp of a DEC CTA has an item in the first round
+// (items = local segments x gws >= warps) but an item never exceeds one load per row per lane.
+// smem: SelectSmem + staged x | idx, xs | partials [ns][gws][256] f32 | residual scales [ns][256].
+bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, Plan* p) {
+  p->n_seg = (d_out + kSegCols - 1) / kSegCols;
+  for (int nd = dec_ctas(warps); nd <= 64; nd *= 2) {
+    const int ns = (p->n_seg + nd - 1) / nd;
+    const int gws_target = (warps + ns - 1) / ns;
+    int rpi = (k_sel + gws_target - 1) / gws_target;
+    if (rpi > max_rpi) rpi = max_rpi;
+    if (rpi < 1) rpi = 1;
+    static int env_rpi = -1;
+    if (env_rpi < 0) {
+      const char* e = getenv("DECDEC_GATHER_ROWS");
+      env_rpi = e ? atoi(e) : 0;
+    }
+    if (env_rpi > 0 && env_rpi < rpi) rpi = env_rpi;
+    const int gws = (k_sel + rpi - 1) / rpi;
+    const uint32_t off_sel = (uint32_t)align_up(select_block_smem_bytes(sel_len), 16);
+    const uint32_t off_part = (uint32_t)align_up((size_t)off_sel + (size_t)k_sel * 6, 16);
+    const uint32_t off_rsc = off_part + (uint32_t)ns * gws * kSegCols * 4;
+    const size_t dec = off_rsc + (size_t)ns * kSegCols * 2;
+    if (dec > kSmemBudget + 16 * 1024) continue;
+    p->n_dec = nd;
+    p->rpi = rpi;
+    p->gws = gws;
+    p->off_sel = off_sel;
+    p->off_part = off_part;
+    p->off_rsc = off_rsc;
+    if (dec > p->smem) p->smem = dec;
+    return true;
+  }
+  return false;
+}
+
+decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int sel_len = 0, int r_bits = 4) {
   if (sel_len == 0) sel_len = d_in;
   const int G = d_in / DECDEC_GROUP;
   const int sms = device_sms();
@@ -64,9 +112,9 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
   Plan best{};
   double best_cost = 1e300;
   bool have = false;
-  for (int nc = 1; nc <= 12; ++nc) {
+  for (int nc = 1; nc <= 16; ++nc) {
     if (small_g ? (nc & (nc - 1)) != 0 : (nc % nkw || ((nc / nkw) & (nc / nkw - 1)) != 0)) continue;
-    for (int rps = 1; rps <= kMaxRPS; rps *= 2) {
+    for (int rps = 1; rps <= kMaxRPS; rps *= 2) {  // rows are computed in pairs: RPS 1 halves the ILP
       if (env_nc > 0 && (nc != env_nc || rps != env_rps)) continue;
       Plan p{};
       p.G = G;
@@ -80,9 +128,8 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
       p.off_z = p.off_s + (uint32_t)p.TR * G * 2;
       p.stage_bytes = (uint32_t)align_up(p.off_z + (uint32_t)p.TR * G, 16);
       const size_t red = (size_t)2 * p.NSLOTS * 4 * (nkw ? nkw : 1) * 4;
-      const size_t sel = align_up((size_t)k_sel * 6, 16);
       const size_t xb = align_up((size_t)d_in * 2, 16);  // staged x (swizzled, see k_linear)
-      const size_t avail = kSmemBudget - red - 16 * 8 - sel - xb;
+      const size_t avail = kSmemBudget - red - 16 * 8 - xb;
       p.stages = (int)(avail / p.stage_bytes);
       if (p.stages > 8) p.stages = 8;
       if (p.stages < 2) continue;
@@ -100,16 +147,17 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
         if (p.stages > cap) p.stages = cap;
       }
       p.n_tiles = d_out / p.TR;
-      // k > 0: the selector CTA(s) take the first SMs; GEMV CTAs fill the rest
-      const int max_grid = k_sel > 0 ? sms - sel_ctas : sms;
-      p.grid = p.n_tiles < max_grid ? p.n_tiles : max_grid;
-      p.NGW = k_sel > 0 ? 2 : 0;
-      p.off_sel = (uint32_t)((size_t)p.stages * p.stage_bytes + red + (size_t)2 * p.stages * 8);
-      p.off_x = (uint32_t)align_up((size_t)p.off_sel + sel, 16);
+      // k > 0: the DEC CTAs take the first SMs; GEMV CTAs fill the rest
+      p.off_x = (uint32_t)align_up((size_t)p.stages * p.stage_bytes + red + (size_t)2 * p.stages * 8, 16);
       p.smem = p.off_x + xb;
-      if (k_sel > 0 && p.smem < select_block_smem_bytes(sel_len)) p.smem = select_block_smem_bytes(sel_len);
-      const double waves = (double)((p.n_tiles + sms - 1) / sms);
-      const double cost = waves * ((double)p.stage_bytes + 3072.0) * (nc < 4 ? 1.0 + 0.15 * (4 - nc) : 1.0);
+      p.n_dec = 0;
+      if (k_sel > 0 && !plan_dec(d_out, k_sel, sel_len, 1 + nc, r_bits == 16 ? kGatherRows16 : kGatherRows4, &p)) continue;
+      const int max_grid = sms - p.n_dec;
+      p.grid = p.n_tiles < max_grid ? p.n_tiles : max_grid;
+      if (p.smem > kSmemBudget + 16 * 1024) continue;
+      const double waves = (double)((p.n_tiles + max_grid - 1) / max_grid);
+      // more consumer warps hide more latency (measured: 16 warps beat 8 by 6-11% on the big layers)
+      const double cost = waves * ((double)p.stage_bytes + 8192.0) * (1.0 + 2.0 / nc) * (rps == 1 ? 1.5 : 1.0);
       if (!have || cost < best_cost * 0.999 || (cost <= best_cost * 1.001 && p.NC > best.NC)) {
         best = p;
         best_cost = cost;
@@ -123,18 +171,15 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
 }
 
 struct WsLayout {
-  size_t cnt, idx, xs, ob, sdev, part, total;
+  size_t cnt, ob, total;
 };
+// workspace: per-segment o_b row counters, then o_b (fp32, d_out)
 WsLayout ws_layout(int k, int d_out) {
+  (void)k;
   WsLayout w{};
   w.cnt = 0;
-  w.idx = align_up((size_t)kCntSlots * 4);
-  w.xs = w.idx + align_up((size_t)k * 4);
-  w.ob = w.xs + align_up((size_t)k * 2);
-  w.sdev = w.ob + align_up((size_t)d_out * 4);
-  w.part = w.sdev + align_up((size_t)d_out * 2);
-  const size_t n_rb = ((size_t)k + kRB - 1) / kRB;
-  w.total = w.part + align_up(n_rb * d_out * 4);
+  w.ob = align_up((size_t)kCntSlots * 4);
+  w.total = w.ob + align_up((size_t)d_out * 4);
   return w;
 }
 
@@ -223,7 +268,7 @@ template <int BITS, int RBITS>
 decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pl.grid);
-  cfg.blockDim = dim3(32 * (1 + pl.NC + pl.NGW));
+  cfg.blockDim = dim3(32 * (1 + pl.NC));
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -260,8 +305,10 @@ LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, 
   p.stage_bytes = pl.stage_bytes;
   p.off_s = pl.off_s;
   p.off_z = pl.off_z;
-  p.NGW = pl.NGW;
+  p.n_dec = pl.n_dec;
   p.off_sel = pl.off_sel;
+  p.off_part = pl.off_part;
+  p.off_rsc = pl.off_rsc;
   p.off_x = pl.off_x;
   p.trace = g_trace ? g_trace + 2 : nullptr;
   static int env_prefetch = -1;
@@ -339,9 +386,8 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
   if (k_sel < 0) return DECDEC_EINVAL;
   if ((s = ensure_attrs()) != DECDEC_OK) return s;
   Prepared P{};
-  const int sel_ctas = k_sel > 0 ? (chunk ? (L->d_in + chunk - 1) / chunk : 1) : 0;
   const int sel_len = chunk ? (chunk < L->d_in ? chunk : L->d_in) : L->d_in;
-  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &P.pl, sel_ctas > 0 ? sel_ctas : 1, sel_len)) != DECDEC_OK)
+  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &P.pl, sel_len, L->r_bits)) != DECDEC_OK)
     return s;
   P.p = base_params(L, x, y, P.pl);
   P.k = k;
@@ -358,29 +404,18 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
     uint8_t* base = static_cast<uint8_t*>(ws);
     LinearParams& p = P.p;
     p.k_sel = k_sel;
-    p.idx = reinterpret_cast<const int*>(base + wl.idx);
-    p.xs = reinterpret_cast<const uint16_t*>(base + wl.xs);
     p.r_rows = static_cast<const uint8_t*>(L->r_rows);
     p.r_scales = L->r_scales;
     p.r_row_bytes = L->d_out * L->r_bits / 8;
     p.ob = reinterpret_cast<float*>(base + wl.ob);
-    p.part = reinterpret_cast<float*>(base + wl.part);
-    p.sdev = reinterpret_cast<uint16_t*>(base + wl.sdev);
     p.cnt = reinterpret_cast<uint32_t*>(base + wl.cnt);
-    p.sel_ready = p.cnt + (kCntSlots - kCtrlSlots);
-    p.cta_done = p.sel_ready + 1;
-    p.sel_ctas = sel_ctas;
     p.k_req = k;
     p.chunk = chunk;
     p.sel_out = sel;
-    p.n_seg = (L->d_out + kSegCols - 1) / kSegCols;
-    if (2 * p.n_seg > kCntSlots - kCtrlSlots) return DECDEC_EUNSUPPORTED;
-    p.n_rb = (k_sel + kRB - 1) / kRB;
-    const int ngw = P.pl.NGW * P.pl.grid;
-    int gws = ngw / p.n_seg;
-    if (gws < 1) gws = 1;
-    if (gws > p.n_rb) gws = p.n_rb;
-    p.gws = gws;
+    p.n_seg = P.pl.n_seg;
+    if (p.n_seg > kCntSlots - kCtrlSlots) return DECDEC_EUNSUPPORTED;
+    p.rpi = P.pl.rpi;
+    p.gws = P.pl.gws;
   }
   *out = P;
   return DECDEC_OK;
@@ -388,7 +423,7 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
 
 decdec_status enqueue_linear(const Prepared& P, cudaStream_t st, bool chained = false) {
   Plan pl = P.pl;
-  pl.grid += P.p.sel_ctas;  // selector CTAs first
+  pl.grid += P.pl.n_dec;  // DEC CTAs first
   return launch_linear(P.p, pl, P.bits, P.p.k_sel ? P.rbits : 4, chained, st);
 }
 
@@ -488,16 +523,16 @@ decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, si
   decdec_status s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &pl);
   if (s != DECDEC_OK) return s;
   snprintf(buf, buf_bytes,
-           "{\"G\": %d, \"NKW\": %d, \"NSLOTS\": %d, \"RPS\": %d, \"TR\": %d, \"NC\": %d, \"NGW\": %d, "
+           "{\"G\": %d, \"NKW\": %d, \"NSLOTS\": %d, \"RPS\": %d, \"TR\": %d, \"NC\": %d, \"n_dec\": %d, "
            "\"stages\": %d, \"stage_bytes\": %u, \"n_tiles\": %d, \"grid\": %d, \"threads\": %d, \"smem\": %zu}",
-           pl.G, pl.NKW, pl.NSLOTS, pl.RPS, pl.TR, pl.NC, pl.NGW, pl.stages, pl.stage_bytes, pl.n_tiles, pl.grid,
-           32 * (1 + pl.NC + pl.NGW), pl.smem);
+           pl.G, pl.NKW, pl.NSLOTS, pl.RPS, pl.TR, pl.NC, pl.n_dec, pl.stages, pl.stage_bytes, pl.n_tiles, pl.grid,
+           32 * (1 + pl.NC), pl.smem);
   return DECDEC_OK;
 }
 
 int32_t decdec_launches_per_call(int32_t k) {
   (void)k;
-  return 1;  // selector CTAs, GEMV and gather run in one kernel
+  return 1;  // DEC CTAs (select + gather + combine) and GEMV CTAs run in one kernel
 }
 
 decdec_status decdec_debug_trace(void* buf, size_t bytes) {

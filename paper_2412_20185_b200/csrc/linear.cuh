@@ -33,15 +33,19 @@
 
 namespace decdec {
 
-constexpr int kRB = 8;            // residual rows per gather work item (in flight per lane)
+constexpr int kGatherRows4 = 32;  // residual rows per gather item, 4-bit R (one u32 per lane per row)
+constexpr int kGatherRows16 = 8;  // ... fp16 R (16 B per lane per row)
 constexpr int kSegCols = 256;     // output columns per combine segment (128 B of 4-bit codes)
-constexpr int kMaxThreads = 480;  // 1 producer + <= 12 consumer + 2 gather warps
+constexpr int kMaxThreads = 544;  // 1 producer + <= 16 consumer warps
 constexpr int kMaxRPS = 4;       // rows per slot per tile
 constexpr int kCntSlots = 4096;   // arrival counters at the head of the workspace
-constexpr int kCtrlSlots = 16;    // last slots of that region: control words (sel_ready, cta_done)
-// trace events (per CTA): 0 start, 1 first TMA issued, 2 x loaded, 3 first stage landed,
-// 4 GEMV done, 5 selector start, 6 selection published, 7 gather done, 8 consumers released (PDL)
-constexpr int kTraceEvents = 9;
+constexpr int kCtrlSlots = 16;    // last slots of that region: reserved control words
+// trace events (per CTA): 0 start, 1 gather done (2nd gather warp), 2 x loaded, 3 first stage landed,
+// 4 GEMV done, 5 selector start, 6 selection published, 7 gather done, 8 consumers released (PDL),
+// 9 last combine done (CTA), 10 last warp exits (CTA), 11 gather warps see the selection,
+// 12 partials published (start), 13 last arrival seen, 14 o_b rows seen, 15 combine loads landed,
+// 16-19 DEC CTA selection phases (x staged, coarse bin, threshold, scan)
+constexpr int kTraceEvents = 20;
 #define DECDEC_TRACE(p, ev)                                                        \
   do {                                                                             \
     if ((p).trace) (p).trace[blockIdx.x * kTraceEvents + (ev)] = globaltimer();    \
@@ -61,61 +65,25 @@ struct LinearParams {
   uint32_t stage_bytes, off_s, off_z;
   // compensation (k_sel == 0: none)
   int k_sel;
-  const int* idx;
-  const uint16_t* xs;
   const uint8_t* r_rows;
   const uint16_t* r_scales;
   int r_row_bytes;
-  float* ob;
-  float* part;
-  uint16_t* sdev;
-  uint32_t* cnt;
-  int n_seg, n_rb, gws, NGW;  // gws = gather warps per segment (each takes row blocks j, j+gws, ...)
-  uint32_t off_sel;            // smem offset of the staged selection (idx int32[k], xs u16[k])
-  uint32_t off_x;              // smem offset of the staged x (d_in fp16, 16-B units swizzled)
-  unsigned long long* trace;   // optional per-CTA event timestamps [grid][kTraceEvents] (ns), or null
-  // step (1) runs on the first sel_ctas CTAs (one per selection segment: the whole x, or one
-  // chunk); each bumps *sel_ready when its indices are written; gather warps wait for
-  // *sel_ready == sel_ctas.  The last CTA to exit resets *sel_ready and *cta_done.
-  int sel_ctas, k_req, chunk;
+  float* ob;      // workspace: fp32 o_b = W_hat x (GEMV CTAs -> DEC combine)
+  uint32_t* cnt;  // workspace: per-segment count of o_b rows written (reset by the combine)
+  int n_seg, gws;  // gws = gather items (partials) per segment
+  int rpi;               // selected rows per gather item (<= kGatherRows4 / kGatherRows16)
+  // smem layout of a DEC CTA: SelectSmem, the staged x segment, idx int32[k_sel], xs u16[k_sel],
+  // partials f32[ns][gws][kSegCols], residual scales u16[ns][kSegCols]
+  uint32_t off_sel, off_part, off_rsc;
+  uint32_t off_x;        // GEMV CTAs: smem offset of the staged x (d_in fp16, 16-B units swizzled)
+  unsigned long long* trace;  // optional per-CTA event timestamps [grid][kTraceEvents] (ns), or null
+  // The first n_dec CTAs are DEC CTAs (steps 1-4): each computes the exact Top-k itself (same
+  // deterministic result in every DEC CTA, no cross-CTA hand-off), keeps S and x[S] in smem and
+  // gathers its share of the (segment, row chunk) items.  The other CTAs run the GEMV.
+  int n_dec, k_req, chunk;
   int prefetch;  // weight tiles requested per CTA before griddepcontrol.wait
   int* sel_out;
-  uint32_t* sel_ready;
-  uint32_t* cta_done;
 };
-
-template <int RBITS>
-__device__ __forceinline__ void combine_segment(const LinearParams& p, int seg, int lane) {
-  const int col0 = seg * kSegCols + lane * 8;
-  if (col0 >= p.d_out) return;
-  const float4 o0 = ld_cg_f4(p.ob + col0), o1 = ld_cg_f4(p.ob + col0 + 4);
-  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int j = 0; j < p.gws; ++j) {  // fixed order: gather warps of the segment ascending
-    const float* pp = p.part + (size_t)j * p.d_out + col0;
-    const float4 a = ld_cg_f4(pp), b = ld_cg_f4(pp + 4);
-    s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
-    s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
-  }
-  float S[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
-  if (RBITS == 4) {
-    const uint4 sv = ld_cg_u4(p.sdev + col0);
-    const uint32_t sw[4] = {sv.x, sv.y, sv.z, sv.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      S[2 * e] = __half2float(__ushort_as_half((unsigned short)(sw[e] & 0xffffu)));
-      S[2 * e + 1] = __half2float(__ushort_as_half((unsigned short)(sw[e] >> 16)));
-    }
-  }
-  const float o[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-  uint32_t out[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const __half lo = __float2half_rn(fmaf(S[2 * e], s[2 * e], o[2 * e]));
-    const __half hi = __float2half_rn(fmaf(S[2 * e + 1], s[2 * e + 1], o[2 * e + 1]));
-    out[e] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
-  }
-  *reinterpret_cast<uint4*>(p.y + col0) = make_uint4(out[0], out[1], out[2], out[3]);
-}
 
 // GEMV side: publish `rows` o_b rows of segment `seg` (caller fenced its stores).
 __device__ __forceinline__ void gemv_publish(const LinearParams& p, int seg, uint32_t rows, int lane) {
@@ -123,43 +91,149 @@ __device__ __forceinline__ void gemv_publish(const LinearParams& p, int seg, uin
   if (lane == 0) atomicAdd(p.cnt + seg, rows);
 }
 
-// Gather side: publish one partial of segment `seg` (caller fenced).  The last of the
-// segment's gws gather warps waits for the segment's o_b rows, combines, and resets both
-// counters for the next call.  Combines are thus spread over the gather warps (one per
-// segment) and never run on the GEMV warps.
+// A DEC CTA (steps 1-4 of P:207).  DEC CTA c owns the output segments c, c + n_dec, ...:
+//   1. every DEC CTA computes the exact Top-k itself (same deterministic result, no hand-off);
+//   2-3. its warps gather the items (local segment, row chunk j) from pinned host memory with
+//        zero-copy loads, double-buffered (the next item's loads are in flight while the
+//        current one is decoded), one fp32 partial per item into smem;
+//   4. after a CTA barrier, a warp per segment waits for the segment's o_b rows (GEMV arrival
+//      count), adds S_j * sum_j part_j in fixed order and writes y.  No global partials, no
+//      value atomics -> deterministic.
 template <int RBITS>
-__device__ __forceinline__ void gather_publish(const LinearParams& p, int seg, int lane) {
-  __syncwarp();
-  uint32_t old = 0;
-  if (lane == 0) old = atomicAdd(p.cnt + p.n_seg + seg, 1u);
-  old = __shfl_sync(0xffffffffu, old, 0);
-  if (old + 1 != (uint32_t)p.gws) return;
-  const uint32_t seg_cols = (uint32_t)min(kSegCols, p.d_out - seg * kSegCols);
-  if (lane == 0) {
-    while (ld_acquire_gpu(p.cnt + seg) != seg_cols) __nanosleep(32);
+__device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, int warp, int lane) {
+  SelectSmem* S = reinterpret_cast<SelectSmem*>(smem);
+  uint4* sx4 = reinterpret_cast<uint4*>(smem + sizeof(SelectSmem));
+  int* sidx = reinterpret_cast<int*>(smem + p.off_sel);
+  uint16_t* sxs = reinterpret_cast<uint16_t*>(sidx + p.k_sel);
+  float* spart = reinterpret_cast<float*>(smem + p.off_part);    // [ns][gws][kSegCols]
+  uint16_t* srsc = reinterpret_cast<uint16_t*>(smem + p.off_rsc);  // [ns][kSegCols] residual scales
+  unsigned long long* tr = p.trace ? p.trace + blockIdx.x * kTraceEvents : nullptr;
+  pdl_wait();  // x may be the previous layer's product; the workspace is the previous layer's
+  if (threadIdx.x == 0) DECDEC_TRACE(p, 5);
+  // ---- step 1: exact Top-k (whole x, or per chunk), S and x[S] into smem
+  const int n_chunks = p.chunk ? (p.d_in + p.chunk - 1) / p.chunk : 1;
+  for (int c = 0; c < n_chunks; ++c) {
+    const int a = p.chunk ? c * p.chunk : 0;
+    const int n = p.chunk ? min(p.chunk, p.d_in - a) : p.d_in;
+    const int q = p.chunk ? min(p.k_req, n) : p.k_req;
+    const int off = p.chunk ? c * p.k_req : 0;  // every earlier chunk is full length >= k
+    select_block(p.x + a, n, q, a, sidx + off, sxs + off,
+                 (blockIdx.x == 0 && p.sel_out) ? p.sel_out + off : nullptr, S, sx4, c == 0 ? tr : nullptr);
+    __syncthreads();  // outputs complete; S / sx4 free for the next chunk
   }
-  __syncwarp();
-  __threadfence();
-  combine_segment<RBITS>(p, seg, lane);
-  if (lane == 0) {
-    p.cnt[seg] = 0;  // ready for the next call
-    p.cnt[p.n_seg + seg] = 0;
-  }
-}
-
-// Called by every warp when it is done (all lanes).  With compensation (k_sel > 0) the last
-// warp of the last CTA resets the PDL-chain control words for the next layer.
-__device__ __forceinline__ void warp_exit(const LinearParams& p, uint32_t* warps_done, int lane) {
-  if (p.k_sel <= 0) return;
-  __syncwarp();
-  if (lane == 0) {
-    if (atomicAdd(warps_done, 1u) == (blockDim.x >> 5) - 1) {       // last warp of this CTA
-      if (atomicAdd(p.cta_done, 1u) == gridDim.x - 1) {               // last CTA of the grid
-        *p.cta_done = 0u;
-        *p.sel_ready = 0u;
+  if (threadIdx.x == 0) DECDEC_TRACE(p, 6);
+  // ---- steps 2-3: gather rows S of R_hat x x[S] for this CTA's segments
+  const int nw = blockDim.x >> 5;
+  const int ns = (p.n_seg - (int)blockIdx.x + p.n_dec - 1) / p.n_dec;  // local segments
+  const int n_items = ns * p.gws;
+  using Vec = typename std::conditional<RBITS == 4, uint32_t, uint4>::type;
+  constexpr int kGR = RBITS == 4 ? kGatherRows4 : kGatherRows16;
+  auto issue = [&](int it, Vec* buf) {  // all zero-copy loads of item `it`
+    const int i = it % ns, j = it / ns;
+    const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
+    const bool cv = col0 < p.d_out;
+    const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
+#pragma unroll
+    for (int r = 0; r < kGR; ++r) {
+      const int e = e0 + r;
+      if (e < e1 && cv) {
+        const uint8_t* rowp = p.r_rows + (size_t)sidx[e] * p.r_row_bytes;
+        if constexpr (RBITS == 4) buf[r] = ld_zc_u32(rowp + (col0 >> 1));
+        else buf[r] = ld_zc_u4(rowp + col0 * 2);
+      } else {
+        if constexpr (RBITS == 4) buf[r] = 0u;
+        else buf[r] = make_uint4(0, 0, 0, 0);
       }
     }
+  };
+  auto consume = [&](int it, const Vec* buf) {  // decode + FHFMA, partial into smem
+    const int i = it % ns, j = it / ns;
+    const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
+    const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
+    if (RBITS == 4 && j == 0 && col0 < p.d_out)  // all scale factors are fetched every call
+      *reinterpret_cast<uint4*>(srsc + i * kSegCols + lane * 8) = ld_zc_u4(p.r_scales + col0);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < kGR; ++r) {
+      const int e = e0 + r;
+      if (e < e1) {
+        const uint16_t xv = sxs[e];
+        uint32_t cq[4];
+        if constexpr (RBITS == 4) {
+          decode_rq_word(buf[r], cq);
+        } else {
+          cq[0] = buf[r].x; cq[1] = buf[r].y; cq[2] = buf[r].z; cq[3] = buf[r].w;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[2 * u] = fhfma_s_lo(xv, cq[u], acc[2 * u]);
+          acc[2 * u + 1] = fhfma_s_hi(xv, cq[u], acc[2 * u + 1]);
+        }
+      }
+    }
+    float* pp = spart + ((size_t)i * p.gws + j) * kSegCols + lane * 8;
+    *reinterpret_cast<float4*>(pp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(pp + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  };
+  {
+    Vec bufA[kGR], bufB[kGR];
+    int it = warp;
+    if (it < n_items) issue(it, bufA);
+    while (it < n_items) {
+      if (it + nw < n_items) issue(it + nw, bufB);
+      consume(it, bufA);
+      it += nw;
+      if (it >= n_items) break;
+      if (it + nw < n_items) issue(it + nw, bufA);
+      consume(it, bufB);
+      it += nw;
+    }
   }
+  if (lane == 0 && (warp == 0 || warp == nw - 1)) DECDEC_TRACE(p, warp == 0 ? 7 : 1);  // gather done
+  __syncthreads();  // all partials of the CTA's segments are in smem
+  if (threadIdx.x == 0) DECDEC_TRACE(p, 12);
+  // ---- step 4: combine, one warp per local segment
+  for (int i = warp; i < ns; i += nw) {
+    const int seg = (int)blockIdx.x + i * p.n_dec;
+    const int col0 = seg * kSegCols + lane * 8;
+    const uint32_t seg_cols = (uint32_t)min(kSegCols, p.d_out - seg * kSegCols);
+    if (lane == 0) {
+      while (ld_acquire_gpu(p.cnt + seg) != seg_cols) __nanosleep(32);  // acquire: the o_b rows
+      if (i == 0) DECDEC_TRACE(p, 14);
+    }
+    __syncwarp();  // orders the lanes' (L2) loads after lane 0's acquire
+    if (col0 < p.d_out) {
+      const float4 o0 = ld_cg_f4(p.ob + col0), o1 = ld_cg_f4(p.ob + col0 + 4);
+      float sum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < p.gws; ++j) {  // fixed order: row chunks ascending
+        const float* pp = spart + ((size_t)i * p.gws + j) * kSegCols + lane * 8;
+        const float4 a = *reinterpret_cast<const float4*>(pp), b = *reinterpret_cast<const float4*>(pp + 4);
+        sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
+        sum[4] += b.x; sum[5] += b.y; sum[6] += b.z; sum[7] += b.w;
+      }
+      float Sc[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
+      if (RBITS == 4) {
+        const uint4 sv = *reinterpret_cast<const uint4*>(srsc + i * kSegCols + lane * 8);
+        const uint32_t sw[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          Sc[2 * e] = __half2float(__ushort_as_half((unsigned short)(sw[e] & 0xffffu)));
+          Sc[2 * e + 1] = __half2float(__ushort_as_half((unsigned short)(sw[e] >> 16)));
+        }
+      }
+      const float o[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+      uint32_t out[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __half lo = __float2half_rn(fmaf(Sc[2 * e], sum[2 * e], o[2 * e]));
+        const __half hi = __float2half_rn(fmaf(Sc[2 * e + 1], sum[2 * e + 1], o[2 * e + 1]));
+        out[e] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+      }
+      *reinterpret_cast<uint4*>(p.y + col0) = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+    if (lane == 0) p.cnt[seg] = 0;  // ready for the next call
+  }
+  if (threadIdx.x == 0) DECDEC_TRACE(p, 9);
 }
 
 template <int BITS, int RBITS>
@@ -170,13 +244,18 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
   uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * p.NSLOTS * 4 * max(p.NKW, 1));
   uint64_t* empty = full + p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ uint32_t warps_done;
   // Let the next kernel of the stream launch now: its CTAs take SMs as ours retire and start
   // streaming their (static) weights while we finish (cross-layer overlap).
   pdl_launch_dependents();
+  if (threadIdx.x == 0) DECDEC_TRACE(p, 0);
 
+  // ------------------------------------------------------------------ DEC CTAs (steps 1-4)
+  if ((int)blockIdx.x < p.n_dec) {
+    dec_cta<RBITS>(p, smem, warp, lane);
+    return;
+  }
+  const int cta = blockIdx.x - p.n_dec, n_cta = gridDim.x - p.n_dec;  // GEMV CTA index / count
   if (threadIdx.x == 0) {
-    warps_done = 0;
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], p.NC);
@@ -184,30 +263,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0) DECDEC_TRACE(p, 0);
-
-  // ------------------------------------------------------------------ selector CTAs (step 1)
-  if ((int)blockIdx.x < p.sel_ctas) {
-    pdl_wait();  // x may be the previous layer's product
-    if (threadIdx.x == 0) DECDEC_TRACE(p, 5);
-    const int seg = blockIdx.x;
-    const int a = p.chunk ? seg * p.chunk : 0;
-    const int n = p.chunk ? min(p.chunk, p.d_in - a) : p.d_in;
-    const int q = p.chunk ? min(p.k_req, n) : p.k_req;
-    const int off = p.chunk ? seg * p.k_req : 0;
-    select_block(p.x + a, n, q, a, const_cast<int*>(p.idx) + off, const_cast<uint16_t*>(p.xs) + off,
-                 p.sel_out ? p.sel_out + off : nullptr, reinterpret_cast<SelectSmem*>(smem),
-                 reinterpret_cast<uint4*>(smem + sizeof(SelectSmem)));
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(p.sel_ready, 1u);
-      DECDEC_TRACE(p, 6);
-    }
-    warp_exit(p, &warps_done, lane);
-    return;
-  }
-  const int cta = blockIdx.x - p.sel_ctas, n_cta = gridDim.x - p.sel_ctas;  // GEMV CTA index / count
 
   // ------------------------------------------------------------------ producer (TMA)
   if (warp == 0) {
@@ -227,14 +282,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
         bulk_g2s(dst, p.w + (size_t)tile * wb, wb, &full[st], pol);
         bulk_g2s(dst + p.off_s, p.ws + (size_t)tile * p.TR * p.G, sb, &full[st], pol);
         bulk_g2s(dst + p.off_z, p.wz + (size_t)tile * p.TR * p.G, zb, &full[st], pol);
-        if (it == 0) DECDEC_TRACE(p, 1);
         if (++st == stages) {
           st = 0;
           ph ^= 1;
         }
       }
     }
-    warp_exit(p, &warps_done, lane);
     return;
   }
 
@@ -317,6 +370,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       const uint16_t* ss = reinterpret_cast<const uint16_t*>(sw + p.off_s);
       const uint8_t* sz = sw + p.off_z;
       float part[4] = {0.f, 0.f, 0.f, 0.f};  // RPS <= 4
+#ifdef DECDEC_SKIP_COMPUTE  // experiment: stream the tiles without computing (memory-bound floor)
+      if (active) part[0] = __half2float(__ushort_as_half(ss[slot * G + g]));
+#else
 #pragma unroll
       for (int m = 0; m < kMaxRPS; m += 2) {
         if (m >= RPS) break;
@@ -371,12 +427,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
           }
         }
       }
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done reading the stage
       int nrows = 0;
       if (small_g) {
         // rows are whole inside the warp: butterfly over the G lanes of each row (fixed order)
-#pragma unroll
         if (G == 32 && RPS == 4) {
           // transposed butterfly: 4 rows in 6 shuffles / 5 dependent rounds (fixed order)
           const bool hi16 = lane & 16, hi8 = lane & 8;
@@ -452,96 +508,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       for (int tile = cta; tile < p.n_tiles; tile += n_cta)
         gemv_publish(p, (tile * TR) / kSegCols, (uint32_t)nrows_tile, lane);
     }
-    warp_exit(p, &warps_done, lane);
     return;
   }
-
-  // ------------------------------------------------------------------ gather warps (DEC)
-  if (p.k_sel <= 0) return;  // (no gather warps are launched without compensation)
-  const int gwi = warp - 1 - p.NC;
-  int* sidx = reinterpret_cast<int*>(smem + p.off_sel);
-  uint16_t* sxs = reinterpret_cast<uint16_t*>(sidx + p.k_sel);
-  pdl_wait();  // the workspace belongs to the previous layer until it completes
-  if (lane == 0) {
-    while (ld_acquire_gpu(p.sel_ready) < (uint32_t)p.sel_ctas) __nanosleep(20);
-  }
-  __syncwarp();
-  for (int i = gwi * 32 + lane; i < p.k_sel; i += p.NGW * 32) {
-    sidx[i] = __ldcg(p.idx + i);
-    sxs[i] = __ldcg(p.xs + i);
-  }
-  named_bar_sync(15, p.NGW * 32);
-  if (gwi == 0 && lane == 0) DECDEC_TRACE(p, 6);
-  const int gw = gwi + p.NGW * cta, ngw = p.NGW * n_cta;
-  for (int pair = gw; pair < p.n_seg * p.gws; pair += ngw) {
-    const int seg = pair % p.n_seg, j = pair / p.n_seg;
-    const int col0 = seg * kSegCols + lane * 8;
-    const bool cv = col0 < p.d_out;
-    if (RBITS == 4 && j == 0 && cv) {  // all scale factors are fetched every call
-      const uint4 sv = ld_zc_u4(p.r_scales + col0);
-      *reinterpret_cast<uint4*>(p.sdev + col0) = sv;
-    }
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    // row blocks rb = j, j + gws, ... (8 rows each), double-buffered: next block's zero-copy
-    // loads are in flight while the current block is decoded.
-    using Vec = typename std::conditional<RBITS == 4, uint32_t, uint4>::type;
-    auto load = [&](int rb, Vec* buf) {
-#pragma unroll
-      for (int r = 0; r < kRB; ++r) {
-        const int e = rb * kRB + r;
-        if (e < p.k_sel && cv) {
-          const uint8_t* rowp = p.r_rows + (size_t)sidx[e] * p.r_row_bytes;
-          if constexpr (RBITS == 4) buf[r] = ld_zc_u32(rowp + (col0 >> 1));
-          else buf[r] = ld_zc_u4(rowp + col0 * 2);
-        } else {
-          if constexpr (RBITS == 4) buf[r] = 0u;
-          else buf[r] = make_uint4(0, 0, 0, 0);
-        }
-      }
-    };
-    auto consume = [&](int rb, const Vec* buf) {
-#pragma unroll
-      for (int r = 0; r < kRB; ++r) {
-        const int e = rb * kRB + r;
-        if (e < p.k_sel) {
-          const uint16_t xv = sxs[e];
-          uint32_t c[4];
-          if constexpr (RBITS == 4) {
-            decode_rq_word(buf[r], c);
-          } else {
-            c[0] = buf[r].x; c[1] = buf[r].y; c[2] = buf[r].z; c[3] = buf[r].w;
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            acc[2 * q] = fhfma_s_lo(xv, c[q], acc[2 * q]);
-            acc[2 * q + 1] = fhfma_s_hi(xv, c[q], acc[2 * q + 1]);
-          }
-        }
-      }
-    };
-    Vec bufA[kRB], bufB[kRB];
-    int rb = j;
-    load(rb, bufA);
-    while (true) {
-      if (rb + p.gws < p.n_rb) load(rb + p.gws, bufB);
-      consume(rb, bufA);
-      rb += p.gws;
-      if (rb >= p.n_rb) break;
-      if (rb + p.gws < p.n_rb) load(rb + p.gws, bufA);
-      consume(rb, bufB);
-      rb += p.gws;
-      if (rb >= p.n_rb) break;
-    }
-    if (cv) {
-      float* pp = p.part + (size_t)j * p.d_out + col0;
-      *reinterpret_cast<float4*>(pp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      *reinterpret_cast<float4*>(pp + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
-    }
-  }
-  if (gwi == 0 && lane == 0) DECDEC_TRACE(p, 7);
-  __threadfence();  // one fence for all of this warp's partials, then the arrivals
-  for (int pair = gw; pair < p.n_seg * p.gws; pair += ngw) gather_publish<RBITS>(p, pair % p.n_seg, lane);
-  warp_exit(p, &warps_done, lane);
 }
 
 // Debug: decode packed weights with the kernel's own decode path; q_out u8 [d_out][d_in].

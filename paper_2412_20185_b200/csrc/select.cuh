@@ -100,7 +100,13 @@ __device__ __forceinline__ uint32_t chunk_elem(const uint4& v, int j) {
 // blocks).
 __device__ __forceinline__ void select_block(const uint16_t* __restrict__ x, int n, int q, int idx_base,
                                              int* __restrict__ idx_out, uint16_t* __restrict__ xs_out,
-                                             int* __restrict__ sel_out, SelectSmem* S, uint4* sx4) {
+                                             int* __restrict__ sel_out, SelectSmem* S, uint4* sx4,
+                                             unsigned long long* tr = nullptr) {
+  // optional phase timestamps (thread 0): [16] x staged, [17] coarse bin, [18] threshold, [19] scan
+#define SEL_TRACE(i)                                  \
+  do {                                                \
+    if (tr && threadIdx.x == 0) tr[i] = globaltimer(); \
+  } while (0)
   const int t = threadIdx.x, NT = blockDim.x, lane = t & 31;
   const int n8 = n >> 3;
   const int C = (n8 + NT - 1) / NT;  // chunks of 8 per thread
@@ -110,6 +116,7 @@ __device__ __forceinline__ void select_block(const uint16_t* __restrict__ x, int
   for (int i = t; i < 256 + 32; i += NT) S->histA[i] = 0;
   for (int i = t; i < 128 + 32; i += NT) S->histB[i] = 0;
   __syncthreads();
+  SEL_TRACE(16);
   const int c0 = t * C, c1 = min(c0 + C, n8);
   // ---- coarse histogram (key >> 7)
 #pragma unroll 1
@@ -129,6 +136,7 @@ __device__ __forceinline__ void select_block(const uint16_t* __restrict__ x, int
     warp_find_bin<8>(c, (uint32_t)q, &S->bA, &S->aboveA);
   }
   __syncthreads();
+  SEL_TRACE(17);
   const uint32_t bA = S->bA, qB = (uint32_t)q - S->aboveA;
   // ---- fine histogram (key & 127) of bin bA
 #pragma unroll 1
@@ -156,6 +164,7 @@ __device__ __forceinline__ void select_block(const uint16_t* __restrict__ x, int
     }
   }
   __syncthreads();
+  SEL_TRACE(18);
   const uint32_t T = S->T;
   const int need = (int)S->need;  // ties (key == T) to take, lowest index first
   // ---- counts, block scan in index order, placement
@@ -171,6 +180,7 @@ __device__ __forceinline__ void select_block(const uint16_t* __restrict__ x, int
     }
   }
   const uint32_t pre = block_exclusive_scan((n_eq << 16) | n_gt, S->tmp);
+  SEL_TRACE(19);
   if (n_gt + n_eq) {
     int eq_seen = (int)(pre >> 16);
     int pos = (int)(pre & 0xffffu) + min(eq_seen, need);
@@ -197,6 +207,7 @@ __device__ __forceinline__ void select_block(const uint16_t* __restrict__ x, int
     }
   }
   (void)lane;
+#undef SEL_TRACE
 }
 
 // Standalone selector (decdec_select): one block per segment.

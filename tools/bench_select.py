@@ -43,7 +43,7 @@ for d_in in (1024, 4096, 14336, 28672):
         print(f"d_in {d_in:6d} k {k:5d}  eager {e0.elapsed_time(e1) * 1e3 / 64:7.2f} us   graph {f0.elapsed_time(f1) * 1e3 / 320:7.2f} us")
 
 # internal timeline of one select (decdec_debug_trace)
-NB = 2 + 1024 * 9
+NB = 2 + 1024 * 20
 buf = torch.zeros(NB, dtype=torch.int64, device="cuda")
 for d_in in (1024, 4096, 14336):
     x = torch.from_numpy(gen_activations(d_in, 1, seed=1)[0]).cuda()
@@ -57,8 +57,8 @@ for d_in in (1024, 4096, 14336):
     dd.decdec_debug_trace(0, 0)
     t = buf.cpu().numpy()
     t0 = t[0]
-    cyc = t[2 + 1024 * 9 - 1] - t[2 + 1024 * 9 - 2]
-    c0 = t[2 + 1024 * 9 - 2]
-    ph = [int(t[2 + 1024 * 9 - 16 + i] - c0) for i in range(6)]
+    cyc = t[2 + 1024 * 20 - 1] - t[2 + 1024 * 20 - 2]
+    c0 = t[2 + 1024 * 20 - 2]
+    ph = [int(t[2 + 1024 * 20 - 16 + i] - c0) for i in range(6)]
     print(d_in, "select us (start->end):", round((t[1] - t0) / 1e3, 2), "cycles", cyc, "=> MHz", round(cyc / ((t[1] - t0) / 1e3)),
           "phase cycles zeroed/hist/T/scan:", ph[:4])

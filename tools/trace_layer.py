@@ -39,7 +39,7 @@ for i in range(a.n):
 k = a.kchunk * d_in // 1024
 ws = dd.Workspace(max(k, 1), d_out)
 y = torch.empty(d_out, dtype=torch.float16, device="cuda")
-NB = 2 + 1024 * 9
+NB = 2 + 1024 * 20
 bufs = [torch.zeros(NB, dtype=torch.int64, device="cuda") for _ in range(a.n)]
 for rep in range(2):
     for i, lin in enumerate(lins):
@@ -54,7 +54,7 @@ print("plan", plan)
 prev_end = None
 for i in range(a.n):
     t = bufs[i].cpu().numpy()
-    ev = t[2: 2 + grid * 9].reshape(grid, 9).astype(np.float64)
+    ev = t[2: 2 + grid * 20].reshape(grid, 20).astype(np.float64)
     base = ev[:, 0][ev[:, 0] > 0].min()
     sel0, sel1 = (ev[0, 5], ev[0, 6]) if k else (0, 0)
     rel = (ev - base) / 1e3

@@ -40,7 +40,8 @@ for b in range(a.blocks):
         meta.append((b, name, d_in, d_out))
 ks = [a.kchunk * m[2] // 1024 for m in meta]
 ws = dd.Workspace(max(max(ks), 1), max(m[3] for m in meta))
-S = 160 * 9
+E = 20
+S = 160 * E
 NB = 2 + len(layers) * S
 buf = torch.zeros(NB, dtype=torch.int64, device="cuda")
 dd.decdec_debug_trace(buf.data_ptr(), NB * 8)
@@ -53,33 +54,53 @@ buf.zero_()
 st.launch()
 torch.cuda.synchronize()
 t = buf.cpu().numpy().astype(np.float64)
-t0 = None
-prev_end = None
-print("layer      start  gemv_done gather_done   end    dur    gap | sel_start sel_pub  released(min/med) x_loaded(med) stage0(med) gemv_done(med)")
+ev_all = [t[2 + i * S: 2 + (i + 1) * S].reshape(160, E) for i in range(len(meta))]
+t0 = min(ev[:, 0][ev[:, 0] > 0].min() for ev in ev_all)
+us = lambda v: (v - t0) / 1e3
+
+
+def med(c):
+    c = c[c > 0]
+    return us(np.median(c)) if len(c) else float("nan")
+
+
+def mx(c):
+    c = c[c > 0]
+    return us(c.max()) if len(c) else float("nan")
+
+
+def mn(c):
+    c = c[c > 0]
+    return us(c.min()) if len(c) else float("nan")
+
+
+print("times in µs from the first layer's start.  GEMV CTAs: released(min) x_loaded(med) gemv_done(max);"
+      "  DEC CTAs: sel_start(med) sel_done(max) gather_done(max) last_arrival(max) combine_done(max);  end, next release")
+ends = []
 for i, (b, name, d_in, d_out) in enumerate(meta):
-    ev = t[2 + i * S: 2 + (i + 1) * S].reshape(160, 9)
-    valid = ev[:, 0] > 0
-    e = ev[valid]
-    start = e[:, 0].min()
-    if t0 is None:
-        t0 = start
-    gemv = e[:, 4][e[:, 4] > 0].max() if (e[:, 4] > 0).any() else start
-    gath = e[:, 7][e[:, 7] > 0].max() if (e[:, 7] > 0).any() else 0
-    end = max(gemv, gath)
-    gap = (start - prev_end) / 1e3 if prev_end is not None else 0.0
-    print(f"{b}:{name:4s} {(start - t0) / 1e3:8.2f} {(gemv - t0) / 1e3:9.2f} {((gath - t0) / 1e3 if gath else 0):9.2f} "
-          f"{(end - t0) / 1e3:8.2f} {(end - start) / 1e3:6.2f} {gap:6.2f}", end="")
-    sel = ev[0] if ks[i] > 0 else None
-    gm = e[1:] if ks[i] > 0 else e
-    extra = ""
-    if sel is not None:
-        extra += f" | {(sel[5] - t0) / 1e3:8.2f} {(sel[6] - t0) / 1e3:7.2f}"
-    else:
-        extra += " |" + " " * 17
-    med = lambda col: np.median(col[col > 0]) if (col > 0).any() else t0
-    rel = gm[:, 8][gm[:, 8] > 0]
-    extra += f"  {(rel.min() - t0) / 1e3 if len(rel) else 0:8.2f} {(med(gm[:, 8]) - t0) / 1e3:8.2f}"
-    extra += f"  xland {(med(gm[:, 5]) - t0) / 1e3:8.2f}"
-    extra += f"  {(med(gm[:, 2]) - t0) / 1e3:8.2f} {(med(gm[:, 3]) - t0) / 1e3:8.2f} {(med(gm[:, 4]) - t0) / 1e3:8.2f}"
-    print(extra)
-    prev_end = end
+    ev = ev_all[i]
+    dec = ev[(ev[:, 5] > 0) & (ev[:, 8] == 0)]
+    gem = ev[ev[:, 8] > 0]
+    end = ev[:, :E].max()
+    ends.append(end)
+    nxt = mn(ev_all[i + 1][:, 8]) if i + 1 < len(meta) else float("nan")
+    line = f"{b}:{name:4s} start {mn(ev[:, 0]):8.2f} | rel {mn(gem[:, 8]):8.2f} x {med(gem[:, 2]):8.2f} gemv {mx(gem[:, 4]):8.2f}"
+    if len(dec):
+        line += (f" | sel {med(dec[:, 5]):8.2f} -> {mx(dec[:, 6]):8.2f} gath {mx(np.maximum(dec[:, 7], dec[:, 1])):8.2f}"
+                 f" arr {mx(dec[:, 13]):8.2f} comb {mx(dec[:, 9]):8.2f}")
+    line += f" | end {us(end):8.2f} next {nxt:8.2f}"
+    print(line)
+nl = len(meta) // a.blocks
+if a.blocks > 1:
+    print(f"last block: {(ends[-1] - ends[-1 - nl]) / 1e3:.2f} us (end to end)")
+rows = []
+for i, (b, name, d_in, d_out) in enumerate(meta):
+    ev = ev_all[i]
+    dec = ev[(ev[:, 5] > 0) & (ev[:, 8] == 0)]
+    if len(dec):
+        d0 = dec[0]
+        rows.append((f"{b}:{name}", [(d0[j] - d0[5]) / 1e3 for j in (16, 17, 18, 19, 6)]))
+if rows:
+    print("DEC CTA 0 selection phases (µs after sel_start): staged, coarse, threshold, scan, done")
+    for n, r in rows[:8]:
+        print(f"  {n:8s}", " ".join(f"{v:6.2f}" for v in r))
