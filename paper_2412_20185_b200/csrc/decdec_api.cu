@@ -46,8 +46,8 @@ constexpr size_t kSmemBudget = 200 * 1024;
 // Launch plan: enumerate (consumer warps NC, rows per slot RPS); pick the one minimising the
 // busiest CTA's bytes (ceil(tiles / SMs) x (stage bytes + a per-tile overhead equivalent)),
 // ties -> more consumer warps.  DECDEC_PLAN="NC,RPS" overrides (tuning).
-// Number of DEC CTAs: enough warps for ~4k zero-copy loads in flight (measured: 128 warps x 32
-// rows saturate PCIe from 4-8 SMs); DECDEC_NDEC overrides.
+// Number of DEC CTAs: ~272 warps of zero-copy loads (measured on the llama3-8b stack at
+// k_chunk 21: 16 DEC CTAs of 17 warps beat 8 by 6%, 4 by 21%); DECDEC_NDEC overrides.
 int dec_ctas(int warps_per_cta) {
   static int env = -1;
   if (env < 0) {
@@ -55,7 +55,7 @@ int dec_ctas(int warps_per_cta) {
     env = e ? atoi(e) : 0;
   }
   if (env > 0) return env;
-  int n = (136 + warps_per_cta - 1) / warps_per_cta;
+  int n = (272 + warps_per_cta - 1) / warps_per_cta;
   return n < 2 ? 2 : (n > 16 ? 16 : n);
 }
 
