@@ -78,7 +78,9 @@ bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, Plan* p
     }
     if (env_rpi > 0 && env_rpi < rpi) rpi = env_rpi;
     const int gws = (k_sel + rpi - 1) / rpi;
-    const uint32_t off_sel = (uint32_t)align_up(select_block_smem_bytes(sel_len), 16);
+    size_t sel_bytes = select_block_smem_bytes(sel_len);
+    if (sel_bytes < sizeof(SelectSmemR)) sel_bytes = sizeof(SelectSmemR);
+    const uint32_t off_sel = (uint32_t)align_up(sel_bytes, 16);
     const uint32_t off_part = (uint32_t)align_up((size_t)off_sel + (size_t)k_sel * 6, 16);
     const uint32_t off_rsc = off_part + (uint32_t)ns * gws * kSegCols * 4;
     const size_t dec = off_rsc + (size_t)ns * kSegCols * 2;

@@ -35,6 +35,7 @@ namespace decdec {
 
 constexpr int kGatherRows4 = 32;  // residual rows per gather item, 4-bit R (one u32 per lane per row)
 constexpr int kGatherRows16 = 8;  // ... fp16 R (16 B per lane per row)
+constexpr int kSelRegChunks = 8;  // register-resident selection: <= 8 chunks of 8 keys per thread
 constexpr int kSegCols = 256;     // output columns per combine segment (128 B of 4-bit codes)
 constexpr int kMaxThreads = 544;  // 1 producer + <= 16 consumer warps
 constexpr int kMaxRPS = 4;       // rows per slot per tile
@@ -103,13 +104,21 @@ template <int RBITS>
 __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, int warp, int lane) {
   SelectSmem* S = reinterpret_cast<SelectSmem*>(smem);
   uint4* sx4 = reinterpret_cast<uint4*>(smem + sizeof(SelectSmem));
+  SelectSmemR* SR = reinterpret_cast<SelectSmemR*>(smem);  // register-resident selector (aliases S)
   int* sidx = reinterpret_cast<int*>(smem + p.off_sel);
   uint16_t* sxs = reinterpret_cast<uint16_t*>(sidx + p.k_sel);
   float* spart = reinterpret_cast<float*>(smem + p.off_part);    // [ns][gws][kSegCols]
   uint16_t* srsc = reinterpret_cast<uint16_t*>(smem + p.off_rsc);  // [ns][kSegCols] residual scales
   unsigned long long* tr = p.trace ? p.trace + blockIdx.x * kTraceEvents : nullptr;
+  const int seg_len = p.chunk ? min(p.chunk, p.d_in) : p.d_in;
+  const bool regs = (seg_len / 8 + (int)blockDim.x - 1) / (int)blockDim.x <= kSelRegChunks;
+  if (regs) select_regs_zero(SR);  // before the wait: smem is ours already
+  __syncthreads();
   pdl_wait();  // x may be the previous layer's product; the workspace is the previous layer's
-  if (threadIdx.x == 0) DECDEC_TRACE(p, 5);
+  if (threadIdx.x == 0) {
+    DECDEC_TRACE(p, 5);
+    if (tr) tr[15] = clock64();  // selection phases 16-19 are SM cycles relative to this
+  }
   // ---- step 1: exact Top-k (whole x, or per chunk), S and x[S] into smem
   const int n_chunks = p.chunk ? (p.d_in + p.chunk - 1) / p.chunk : 1;
   for (int c = 0; c < n_chunks; ++c) {
@@ -117,11 +126,17 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     const int n = p.chunk ? min(p.chunk, p.d_in - a) : p.d_in;
     const int q = p.chunk ? min(p.k_req, n) : p.k_req;
     const int off = p.chunk ? c * p.k_req : 0;  // every earlier chunk is full length >= k
-    select_block(p.x + a, n, q, a, sidx + off, sxs + off,
-                 (blockIdx.x == 0 && p.sel_out) ? p.sel_out + off : nullptr, S, sx4, c == 0 ? tr : nullptr);
-    __syncthreads();  // outputs complete; S / sx4 free for the next chunk
+    int* so = (blockIdx.x == 0 && p.sel_out) ? p.sel_out + off : nullptr;
+    if (regs)
+      select_block_regs_any(p.x + a, n, q, a, sidx + off, sxs + off, so, SR, c == 0 ? tr : nullptr);
+    else
+      select_block(p.x + a, n, q, a, sidx + off, sxs + off, so, S, sx4, c == 0 ? tr : nullptr);
+    __syncthreads();  // outputs complete; the selector scratch is free for the next chunk
   }
-  if (threadIdx.x == 0) DECDEC_TRACE(p, 6);
+  if (threadIdx.x == 0) {
+    DECDEC_TRACE(p, 6);
+    if (tr) tr[14] = clock64();
+  }
   // ---- steps 2-3: gather rows S of R_hat x x[S] for this CTA's segments
   const int nw = blockDim.x >> 5;
   const int ns = (p.n_seg - (int)blockIdx.x + p.n_dec - 1) / p.n_dec;  // local segments
@@ -199,7 +214,6 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     const uint32_t seg_cols = (uint32_t)min(kSegCols, p.d_out - seg * kSegCols);
     if (lane == 0) {
       while (ld_acquire_gpu(p.cnt + seg) != seg_cols) __nanosleep(32);  // acquire: the o_b rows
-      if (i == 0) DECDEC_TRACE(p, 14);
     }
     __syncwarp();  // orders the lanes' (L2) loads after lane 0's acquire
     if (col0 < p.d_out) {

@@ -1,0 +1,60 @@
+// Cost of the DEC CTA's exact Top-k (select_block_regs) in isolation: one CTA, `iters` calls
+// back to back on the same x (instruction cache and L1 warm), thread 0 records SM cycles per
+// phase into a trace array.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cmath>
+#include "select.cuh"
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { fprintf(stderr, "CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); return 1;} } while (0)
+using namespace decdec;
+
+__global__ void k_sel(const uint16_t* x, int n, int q, int iters, int* idx, uint16_t* xs, unsigned long long* tr) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  SelectSmemR* S = reinterpret_cast<SelectSmemR*>(smem);
+  int* sidx = reinterpret_cast<int*>(smem + sizeof(SelectSmemR));
+  uint16_t* sxs = reinterpret_cast<uint16_t*>(sidx + q);
+  select_regs_zero(S);
+  __syncthreads();
+  for (int it = 0; it < iters; ++it) {
+    unsigned long long* t = tr + it * 20;
+    if (threadIdx.x == 0) t[15] = clock64();
+    select_block_regs_any(x, n, q, 0, sidx, sxs, nullptr, S, t);
+    __syncthreads();
+    if (threadIdx.x == 0) t[14] = clock64();
+  }
+  for (int i = threadIdx.x; i < q; i += blockDim.x) { idx[i] = sidx[i]; xs[i] = sxs[i]; }
+}
+
+int main() {
+  for (int n : {4096, 14336}) {
+    for (int nt : {288, 544}) {
+      const int q = n / 1024 * 21;
+      uint16_t* hx = (uint16_t*)malloc(n * 2);
+      srand(5);
+      for (int i = 0; i < n; ++i) {
+        float g = 0; for (int k = 0; k < 12; ++k) g += rand() / (float)RAND_MAX; g -= 6;
+        float v = expf(0.5f * g) * (rand() & 1 ? 1 : -1) * 0.3f;
+        __half h = __float2half(v); hx[i] = *reinterpret_cast<uint16_t*>(&h);
+      }
+      uint16_t *dx, *dxs; int* didx; unsigned long long* dtr;
+      const int iters = getenv("ITERS") ? atoi(getenv("ITERS")) : 20;
+      CK(cudaMalloc(&dx, n * 2)); CK(cudaMalloc(&didx, q * 4)); CK(cudaMalloc(&dxs, q * 2)); CK(cudaMalloc(&dtr, iters * 20 * 8));
+      CK(cudaMemcpy(dx, hx, n * 2, cudaMemcpyHostToDevice));
+      const size_t sm = sizeof(SelectSmemR) + q * 6 + 64;
+      CK(cudaFuncSetAttribute(k_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_sel<<<1, nt, sm>>>(dx, n, q, iters, didx, dxs, dtr);
+      CK(cudaDeviceSynchronize());
+      static unsigned long long h[1000 * 20];
+      CK(cudaMemcpy(h, dtr, iters * 20 * 8, cudaMemcpyDeviceToHost));
+      for (int it : {0, 1, iters - 1}) {
+        unsigned long long* t = h + it * 20;
+        printf("{\"n\": %d, \"threads\": %d, \"iter\": %d, \"cycles\": [%lld, %lld, %lld, %lld, %lld]}\n", n, nt, it,
+               (long long)(t[16] - t[15]), (long long)(t[17] - t[15]), (long long)(t[18] - t[15]), (long long)(t[19] - t[15]),
+               (long long)(t[14] - t[15]));
+      }
+    }
+  }
+  return 0;
+}

@@ -210,6 +210,210 @@ __device__ __forceinline__ void select_block(const uint16_t* __restrict__ x, int
 #undef SEL_TRACE
 }
 
+
+// ---------------------------------------------------------------- register-resident variant
+// Same result as select_block, for a block whose threads can hold the whole segment in
+// registers (ceil(n / 8 / blockDim) <= MAXC chunks of 8 keys each).  Latency-oriented: three
+// block barriers in total, no single-warp serial sections (every warp derives the bin /
+// threshold / its output offset redundantly from shared counters), no smem staging pass, the
+// coarse histogram split in 4 copies (lane & 3) against same-bin lane conflicts.  The caller
+// zeroes S once before the first call (select_regs_zero + __syncthreads, e.g. before
+// griddepcontrol.wait); each call leaves S zeroed again after its last barrier... except for
+// the final zeroing, which the caller's barrier after the call orders before the next call.
+struct SelectSmemR {
+  uint32_t histA[4][256 + 32];  // copy c, bin b at b + (b >> 3)
+  uint32_t histB[128 + 32];     // bin b at b + (b >> 2)
+  uint32_t wsum[kSelMaxWarps];  // per-warp (n_eq << 16 | n_gt) totals
+};
+__device__ __forceinline__ void select_regs_zero(SelectSmemR* S) {
+  uint32_t* h = &S->histA[0][0];
+  for (int i = threadIdx.x; i < 4 * (256 + 32) + 128 + 32; i += blockDim.x) h[i] = 0u;
+}
+
+// warp-redundant version of warp_find_bin: every lane gets (bin, above) for the q-th largest
+template <int PER>
+__device__ __forceinline__ void warp_find_bin_all(const uint32_t* c, uint32_t q, uint32_t* bin, uint32_t* above_out) {
+  const int lane = threadIdx.x & 31;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) sum += c[j];
+  const uint32_t sr = __shfl_sync(0xffffffffu, sum, 31 - lane);
+  uint32_t inc = sr;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  const uint32_t above = __shfl_sync(0xffffffffu, inc, 31 - lane) - sum;  // keys in lanes > l
+  uint32_t b = 0, ab = 0;
+  const bool mine = above < q && above + sum >= q;
+  if (mine) {
+    uint32_t run = above;
+#pragma unroll
+    for (int j = PER - 1; j >= 0; --j) {
+      if (run + c[j] >= q) {
+        b = (uint32_t)(PER * lane + j);
+        ab = run;
+        break;
+      }
+      run += c[j];
+    }
+  }
+  const uint32_t who = __ballot_sync(0xffffffffu, mine);
+  const int src = who ? __ffs(who) - 1 : 0;
+  *bin = __shfl_sync(0xffffffffu, b, src);
+  *above_out = __shfl_sync(0xffffffffu, ab, src);
+}
+
+template <int MAXC>
+__device__ __forceinline__ void select_block_regs(const uint16_t* __restrict__ x, int n, int q, int idx_base,
+                                                  int* __restrict__ idx_out, uint16_t* __restrict__ xs_out,
+                                                  int* __restrict__ sel_out, SelectSmemR* S,
+                                                  unsigned long long* tr = nullptr) {
+#define SEL_TRACE(i)                                  \
+  do {                                                \
+    if (tr && threadIdx.x == 0) tr[i] = clock64();     \
+  } while (0)
+  const int t = threadIdx.x, NT = blockDim.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
+  const int n8 = n >> 3;
+  const int C = (n8 + NT - 1) / NT;  // <= MAXC (caller's guarantee)
+  const int c0 = t * C;
+  const int nv = max(0, min(C, n8 - c0));  // valid chunks of this thread
+  uint4 v[MAXC];
+  const uint4* x4 = reinterpret_cast<const uint4*>(x) + c0;
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) v[m] = m < nv ? __ldg(x4 + m) : make_uint4(0, 0, 0, 0);
+  SEL_TRACE(16);
+  // ---- coarse histogram (key >> 7), 4 copies
+  uint32_t* hA = S->histA[lane & 3];
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) {
+    if (m < nv) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t b = (chunk_elem(v[m], j) & 0x7fffu) >> 7;
+        atomicAdd(&hA[b + (b >> 3)], 1u);
+      }
+    }
+  }
+  __syncthreads();  // barrier 1
+  uint32_t bA, aboveA;
+  {
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      c[j] = S->histA[0][9 * lane + j] + S->histA[1][9 * lane + j] + S->histA[2][9 * lane + j] + S->histA[3][9 * lane + j];
+    warp_find_bin_all<8>(c, (uint32_t)q, &bA, &aboveA);
+  }
+  SEL_TRACE(17);
+  const uint32_t qB = (uint32_t)q - aboveA;
+  // ---- fine histogram (key & 127) of bin bA
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) {
+    if (m < nv) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t key = chunk_elem(v[m], j) & 0x7fffu;
+        if ((key >> 7) == bA) {
+          const uint32_t b = key & 127u;
+          atomicAdd(&S->histB[b + (b >> 2)], 1u);
+        }
+      }
+    }
+  }
+  __syncthreads();  // barrier 2
+  uint32_t T, need_u;
+  {
+    uint32_t c[4], bin, above;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[j] = S->histB[5 * lane + j];
+    warp_find_bin_all<4>(c, qB, &bin, &above);
+    T = (bA << 7) | bin;
+    need_u = qB - above;
+  }
+  SEL_TRACE(18);
+  const int need = (int)need_u;  // ties (key == T) to take, lowest index first
+  // ---- counts, block scan in index order (one barrier), placement
+  uint32_t n_gt = 0, n_eq = 0;
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) {
+    if (m < nv) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t key = chunk_elem(v[m], j) & 0x7fffu;
+        n_gt += key > T;
+        n_eq += key == T;
+      }
+    }
+  }
+  const uint32_t mine = (n_eq << 16) | n_gt;
+  uint32_t inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) S->wsum[wid] = inc;
+  __syncthreads();  // barrier 3: histograms are no longer read, warp totals are visible
+  uint32_t wpre;
+  {
+    const uint32_t wt = lane < nw ? S->wsum[lane] : 0u;
+    uint32_t wi = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    wpre = __shfl_sync(0xffffffffu, wi - wt, wid);  // exclusive prefix of this warp
+  }
+  SEL_TRACE(19);
+  {  // zero the histograms for the next call (the caller's barrier orders it before that call)
+    uint32_t* h = &S->histA[0][0];
+    for (int i = t; i < 4 * (256 + 32) + 128 + 32; i += NT) h[i] = 0u;
+  }
+  const uint32_t pre = wpre + inc - mine;
+  if (n_gt + n_eq) {
+    int eq_seen = (int)(pre >> 16);
+    int pos = (int)(pre & 0xffffu) + min(eq_seen, need);
+#pragma unroll
+    for (int m = 0; m < MAXC; ++m) {
+      if (m < nv) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t raw = chunk_elem(v[m], j);
+          const uint32_t key = raw & 0x7fffu;
+          bool take = key > T;
+          if (key == T) {
+            take = eq_seen < need;
+            ++eq_seen;
+          }
+          if (take) {
+            const int i = idx_base + 8 * (c0 + m) + j;
+            idx_out[pos] = i;
+            xs_out[pos] = (uint16_t)raw;
+            if (sel_out) sel_out[pos] = i;
+            ++pos;
+          }
+        }
+      }
+    }
+  }
+#undef SEL_TRACE
+}
+
+// Dispatch on the chunks per thread (fewer unrolled slots -> less predication overhead).
+__device__ __forceinline__ bool select_block_regs_any(const uint16_t* x, int n, int q, int idx_base, int* idx_out,
+                                                      uint16_t* xs_out, int* sel_out, SelectSmemR* S,
+                                                      unsigned long long* tr) {
+  const int C = ((n >> 3) + (int)blockDim.x - 1) / (int)blockDim.x;
+  if (C <= 1) select_block_regs<1>(x, n, q, idx_base, idx_out, xs_out, sel_out, S, tr);
+  else if (C <= 2) select_block_regs<2>(x, n, q, idx_base, idx_out, xs_out, sel_out, S, tr);
+  else if (C <= 4) select_block_regs<4>(x, n, q, idx_base, idx_out, xs_out, sel_out, S, tr);
+  else if (C <= 8) select_block_regs<8>(x, n, q, idx_base, idx_out, xs_out, sel_out, S, tr);
+  else return false;
+  return true;
+}
+
 // Standalone selector (decdec_select): one block per segment.
 __global__ void __launch_bounds__(1024) k_select(const uint16_t* __restrict__ x, int d_in, int k, int chunk,
                                                  int* __restrict__ idx_out, uint16_t* __restrict__ xs_out,

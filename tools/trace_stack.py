@@ -99,8 +99,8 @@ for i, (b, name, d_in, d_out) in enumerate(meta):
     dec = ev[(ev[:, 5] > 0) & (ev[:, 8] == 0)]
     if len(dec):
         d0 = dec[0]
-        rows.append((f"{b}:{name}", [(d0[j] - d0[5]) / 1e3 for j in (16, 17, 18, 19, 6)]))
+        rows.append((f"{b}:{name}", [d0[j] - d0[15] for j in (16, 17, 18, 19, 14)]))
 if rows:
-    print("DEC CTA 0 selection phases (µs after sel_start): staged, coarse, threshold, scan, done")
+    print("DEC CTA 0 selection phases (SM cycles after sel_start): loads issued, coarse bin, threshold, scan, done")
     for n, r in rows[:8]:
-        print(f"  {n:8s}", " ".join(f"{v:6.2f}" for v in r))
+        print(f"  {n:8s}", " ".join(f"{v:7.0f}" for v in r))
