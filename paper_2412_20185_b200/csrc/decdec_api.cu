@@ -37,7 +37,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 struct Plan {
   int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, n_dec;  // grid = GEMV CTAs (+ n_dec DEC CTAs)
   int n_seg, rpi, gws;  // DEC: output segments, selected rows per gather item, items per segment
-  uint32_t stage_bytes, off_s, off_z, off_sel, off_x, off_part, off_rsc;
+  uint32_t stage_bytes, off_s, off_z, off_sel, off_x, off_part, off_rsc, off_stage;
   size_t smem;
 };
 
@@ -79,11 +79,12 @@ bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, Plan* p
     if (env_rpi > 0 && env_rpi < rpi) rpi = env_rpi;
     const int gws = (k_sel + rpi - 1) / rpi;
     size_t sel_bytes = select_block_smem_bytes(sel_len);
-    if (sel_bytes < sizeof(SelectSmemR)) sel_bytes = sizeof(SelectSmemR);
+    if (sel_bytes < select_split_smem_bytes(sel_len)) sel_bytes = select_split_smem_bytes(sel_len);
     const uint32_t off_sel = (uint32_t)align_up(sel_bytes, 16);
     const uint32_t off_part = (uint32_t)align_up((size_t)off_sel + (size_t)k_sel * 6, 16);
     const uint32_t off_rsc = off_part + (uint32_t)ns * gws * kSegCols * 4;
-    const size_t dec = off_rsc + (size_t)ns * kSegCols * 2;
+    const uint32_t off_stage = (uint32_t)align_up((size_t)off_rsc + (size_t)ns * kSegCols * 2, 16);
+    const size_t dec = off_stage + (size_t)warps * 2 * 32 * 128;  // kGatherRows4 x u32 = kGatherRows16 x 16 B
     if (dec > kSmemBudget + 16 * 1024) continue;
     p->n_dec = nd;
     p->rpi = rpi;
@@ -91,6 +92,7 @@ bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, Plan* p
     p->off_sel = off_sel;
     p->off_part = off_part;
     p->off_rsc = off_rsc;
+    p->off_stage = off_stage;
     if (dec > p->smem) p->smem = dec;
     return true;
   }
@@ -311,6 +313,7 @@ LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, 
   p.off_sel = pl.off_sel;
   p.off_part = pl.off_part;
   p.off_rsc = pl.off_rsc;
+  p.off_stage = pl.off_stage;
   p.off_x = pl.off_x;
   p.trace = g_trace ? g_trace + 2 : nullptr;
   static int env_prefetch = -1;

@@ -39,6 +39,9 @@ constexpr int kSelRegChunks = 8;  // register-resident selection: <= 8 chunks of
 constexpr int kSegCols = 256;     // output columns per combine segment (128 B of 4-bit codes)
 constexpr int kMaxThreads = 544;  // 1 producer + <= 16 consumer warps
 constexpr int kMaxRPS = 4;       // rows per slot per tile
+#ifndef DECDEC_ROW_STEP
+#define DECDEC_ROW_STEP 2  // consumer rows per inner step: 2 (row pairs, more ILP) or 1 (smaller loop)
+#endif
 constexpr int kCntSlots = 4096;   // arrival counters at the head of the workspace
 constexpr int kCtrlSlots = 16;    // last slots of that region: reserved control words
 // trace events (per CTA): 0 start, 1 gather done (2nd gather warp), 2 x loaded, 3 first stage landed,
@@ -75,7 +78,7 @@ struct LinearParams {
   int rpi;               // selected rows per gather item (<= kGatherRows4 / kGatherRows16)
   // smem layout of a DEC CTA: SelectSmem, the staged x segment, idx int32[k_sel], xs u16[k_sel],
   // partials f32[ns][gws][kSegCols], residual scales u16[ns][kSegCols]
-  uint32_t off_sel, off_part, off_rsc;
+  uint32_t off_sel, off_part, off_rsc, off_stage;  // ... + per-warp gather staging [warps][2][rows][32]
   uint32_t off_x;        // GEMV CTAs: smem offset of the staged x (d_in fp16, 16-B units swizzled)
   unsigned long long* trace;  // optional per-CTA event timestamps [grid][kTraceEvents] (ns), or null
   // The first n_dec CTAs are DEC CTAs (steps 1-4): each computes the exact Top-k itself (same
@@ -105,6 +108,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   SelectSmem* S = reinterpret_cast<SelectSmem*>(smem);
   uint4* sx4 = reinterpret_cast<uint4*>(smem + sizeof(SelectSmem));
   SelectSmemR* SR = reinterpret_cast<SelectSmemR*>(smem);  // register-resident selector (aliases S)
+  SelectSmemS* SS = reinterpret_cast<SelectSmemS*>(smem);  // split-order selector (aliases S)
   int* sidx = reinterpret_cast<int*>(smem + p.off_sel);
   uint16_t* sxs = reinterpret_cast<uint16_t*>(sidx + p.k_sel);
   float* spart = reinterpret_cast<float*>(smem + p.off_part);    // [ns][gws][kSegCols]
@@ -112,72 +116,58 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   unsigned long long* tr = p.trace ? p.trace + blockIdx.x * kTraceEvents : nullptr;
   const int seg_len = p.chunk ? min(p.chunk, p.d_in) : p.d_in;
   const bool regs = (seg_len / 8 + (int)blockDim.x - 1) / (int)blockDim.x <= kSelRegChunks;
-  if (regs) select_regs_zero(SR);  // before the wait: smem is ours already
+  const bool split = !p.chunk && regs && p.d_in <= 32 * 1024;
+  if (split) select_split_zero(SS, p.d_in);  // before the wait: smem is ours already
+  else if (regs) select_regs_zero(SR);
   __syncthreads();
   pdl_wait();  // x may be the previous layer's product; the workspace is the previous layer's
   if (threadIdx.x == 0) {
     DECDEC_TRACE(p, 5);
     if (tr) tr[15] = clock64();  // selection phases 16-19 are SM cycles relative to this
   }
-  // ---- step 1: exact Top-k (whole x, or per chunk), S and x[S] into smem
-  const int n_chunks = p.chunk ? (p.d_in + p.chunk - 1) / p.chunk : 1;
-  for (int c = 0; c < n_chunks; ++c) {
-    const int a = p.chunk ? c * p.chunk : 0;
-    const int n = p.chunk ? min(p.chunk, p.d_in - a) : p.d_in;
-    const int q = p.chunk ? min(p.k_req, n) : p.k_req;
-    const int off = p.chunk ? c * p.k_req : 0;  // every earlier chunk is full length >= k
-    int* so = (blockIdx.x == 0 && p.sel_out) ? p.sel_out + off : nullptr;
-    if (regs)
-      select_block_regs_any(p.x + a, n, q, a, sidx + off, sxs + off, so, SR, c == 0 ? tr : nullptr);
-    else
-      select_block(p.x + a, n, q, a, sidx + off, sxs + off, so, S, sx4, c == 0 ? tr : nullptr);
-    __syncthreads();  // outputs complete; the selector scratch is free for the next chunk
-  }
-  if (threadIdx.x == 0) {
-    DECDEC_TRACE(p, 6);
-    if (tr) tr[14] = clock64();
-  }
-  // ---- steps 2-3: gather rows S of R_hat x x[S] for this CTA's segments
   const int nw = blockDim.x >> 5;
   const int ns = (p.n_seg - (int)blockIdx.x + p.n_dec - 1) / p.n_dec;  // local segments
   const int n_items = ns * p.gws;
   using Vec = typename std::conditional<RBITS == 4, uint32_t, uint4>::type;
   constexpr int kGR = RBITS == 4 ? kGatherRows4 : kGatherRows16;
-  auto issue = [&](int it, Vec* buf) {  // all zero-copy loads of item `it`
+  // per-warp staging: 2 buffers x kGR rows x 32 lanes x Vec (cp.async destinations)
+  Vec* stage = reinterpret_cast<Vec*>(smem + p.off_stage) + (size_t)warp * 2 * kGR * 32;
+  auto issue = [&](int it, int bsel) {  // all zero-copy reads of item `it` (async, into smem)
     const int i = it % ns, j = it / ns;
     const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
     const bool cv = col0 < p.d_out;
     const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
+    Vec* dst = stage + bsel * kGR * 32 + lane;
 #pragma unroll
     for (int r = 0; r < kGR; ++r) {
       const int e = e0 + r;
       if (e < e1 && cv) {
         const uint8_t* rowp = p.r_rows + (size_t)sidx[e] * p.r_row_bytes;
-        if constexpr (RBITS == 4) buf[r] = ld_zc_u32(rowp + (col0 >> 1));
-        else buf[r] = ld_zc_u4(rowp + col0 * 2);
-      } else {
-        if constexpr (RBITS == 4) buf[r] = 0u;
-        else buf[r] = make_uint4(0, 0, 0, 0);
+        if constexpr (RBITS == 4) cp_async_4(dst + r * 32, rowp + (col0 >> 1));
+        else cp_async_16(dst + r * 32, rowp + col0 * 2);
       }
     }
+    cp_async_commit();
   };
-  auto consume = [&](int it, const Vec* buf) {  // decode + FHFMA, partial into smem
+  auto consume = [&](int it, int bsel) {  // decode + FHFMA, partial into smem
     const int i = it % ns, j = it / ns;
     const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
     const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
     if (RBITS == 4 && j == 0 && col0 < p.d_out)  // all scale factors are fetched every call
       *reinterpret_cast<uint4*>(srsc + i * kSegCols + lane * 8) = ld_zc_u4(p.r_scales + col0);
+    const Vec* src = stage + bsel * kGR * 32 + lane;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int r = 0; r < kGR; ++r) {
       const int e = e0 + r;
       if (e < e1) {
         const uint16_t xv = sxs[e];
+        const Vec w = src[r * 32];
         uint32_t cq[4];
         if constexpr (RBITS == 4) {
-          decode_rq_word(buf[r], cq);
+          decode_rq_word(w, cq);
         } else {
-          cq[0] = buf[r].x; cq[1] = buf[r].y; cq[2] = buf[r].z; cq[3] = buf[r].w;
+          cq[0] = w.x; cq[1] = w.y; cq[2] = w.z; cq[3] = w.w;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -190,19 +180,59 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     *reinterpret_cast<float4*>(pp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     *reinterpret_cast<float4*>(pp + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
   };
-  {
-    Vec bufA[kGR], bufB[kGR];
-    int it = warp;
-    if (it < n_items) issue(it, bufA);
-    while (it < n_items) {
-      if (it + nw < n_items) issue(it + nw, bufB);
-      consume(it, bufA);
-      it += nw;
-      if (it >= n_items) break;
-      if (it + nw < n_items) issue(it + nw, bufA);
-      consume(it, bufB);
-      it += nw;
+  int it = warp;
+  // ---- step 1: exact Top-k (whole x, or per chunk), S and x[S] into smem.  In global mode the
+  // rows whose coarse bin is above the threshold bin (positions [0, nD)) are known after three
+  // block barriers; the last warp finishes the rest alone while the others start gathering.
+  int nD = -1;
+  if (split) {
+    nD = select_split_any(p.x, p.d_in, p.k_req, sidx, sxs, blockIdx.x == 0 ? p.sel_out : nullptr, SS, nw - 1, tr);
+#ifdef DECDEC_SPLIT_SERIAL
+    __syncthreads();  // experiment switch: wait for the finisher before any gather
+    if (nD >= 0) nD = p.k_sel;
+#endif
+  }
+  if (nD < 0) {
+    const int n_chunks = p.chunk ? (p.d_in + p.chunk - 1) / p.chunk : 1;
+    for (int c = 0; c < n_chunks; ++c) {
+      const int a = p.chunk ? c * p.chunk : 0;
+      const int n = p.chunk ? min(p.chunk, p.d_in - a) : p.d_in;
+      const int q = p.chunk ? min(p.k_req, n) : p.k_req;
+      const int off = p.chunk ? c * p.k_req : 0;  // every earlier chunk is full length >= k
+      int* so = (blockIdx.x == 0 && p.sel_out) ? p.sel_out + off : nullptr;
+      if (regs)
+        select_block_regs_any(p.x + a, n, q, a, sidx + off, sxs + off, so, SR, c == 0 ? tr : nullptr);
+      else
+        select_block(p.x + a, n, q, a, sidx + off, sxs + off, so, S, sx4, c == 0 ? tr : nullptr);
+      __syncthreads();  // outputs complete; the selector scratch is free for the next chunk
     }
+    nD = p.k_sel;
+  }
+  bool rest_seen = nD >= p.k_sel;
+  auto ready = [&](int item) {  // the rows of `item` are placed
+    if (!rest_seen && min((item / ns) * p.rpi + p.rpi, p.k_sel) > nD) {
+      select_wait_rest(SS);
+      rest_seen = true;
+    }
+  };
+  if (threadIdx.x == 0) {
+    DECDEC_TRACE(p, 6);
+    if (tr) tr[14] = clock64();
+  }
+  // ---- steps 2-3: gather rows S of R_hat x x[S] for this CTA's segments (double-buffered)
+  if (it < n_items) {
+    ready(it);
+    issue(it, 0);
+  }
+  for (int b = 0; it < n_items; b ^= 1, it += nw) {
+    if (it + nw < n_items) {
+      ready(it + nw);
+      issue(it + nw, b ^ 1);
+      cp_async_wait<1>();  // this item's group has landed (the next one may be in flight)
+    } else {
+      cp_async_wait<0>();
+    }
+    consume(it, b);
   }
   if (lane == 0 && (warp == 0 || warp == nw - 1)) DECDEC_TRACE(p, warp == 0 ? 7 : 1);  // gather done
   __syncthreads();  // all partials of the CTA's segments are in smem
@@ -387,6 +417,47 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
 #ifdef DECDEC_SKIP_COMPUTE  // experiment: stream the tiles without computing (memory-bound floor)
       if (active) part[0] = __half2float(__ushort_as_half(ss[slot * G + g]));
 #else
+#if DECDEC_ROW_STEP == 1
+      // one row per step, rolled over the tile's RPS rows: the loop body (~3.5 KB of SASS for
+      // 3-bit) stays inside the ~6 KB L0 instruction cache with the tile bookkeeping
+#pragma unroll 1
+      for (int m = 0; m < RPS; ++m) {
+        const int r0 = slot + m * NSLOTS;
+        if (active) {
+          const uint8_t* g0 = sw + r0 * row_bytes + g * GB;
+          float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (BITS == 4) {
+            uint4 v0[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v0[j] = *reinterpret_cast<const uint4*>(g0 + 16 * ((j + rot) & 3));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              fma_w4_word(v0[j].x, xr + 16 * j + 0, a0);
+              fma_w4_word(v0[j].y, xr + 16 * j + 4, a0);
+              fma_w4_word(v0[j].z, xr + 16 * j + 8, a0);
+              fma_w4_word(v0[j].w, xr + 16 * j + 12, a0);
+            }
+          } else {
+            uint32_t w0[12];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const uint4 t0 = *reinterpret_cast<const uint4*>(g0 + 16 * j);
+              w0[4 * j] = t0.x; w0[4 * j + 1] = t0.y; w0[4 * j + 2] = t0.z; w0[4 * j + 3] = t0.w;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) fma_w3_slice(w0[3 * u], w0[3 * u + 1], w0[3 * u + 2], xr + 16 * u, a0);
+          }
+          const float t0 = combine_classes<BITS>(a0);
+          const float s0 = __half2float(__ushort_as_half(ss[r0 * G + g])) * 16777216.f;  // s * 2^24
+          const float z0 = (float)sz[r0 * G + g];
+          const float v = s0 * fmaf(-z0, Xs, t0);  // s * sum_(i in g) (q_i - z) x_i
+          part[0] = m == 0 ? v : part[0];
+          part[1] = m == 1 ? v : part[1];
+          part[2] = m == 2 ? v : part[2];
+          part[3] = m == 3 ? v : part[3];
+        }
+      }
+#else
 #pragma unroll
       for (int m = 0; m < kMaxRPS; m += 2) {
         if (m >= RPS) break;
@@ -441,7 +512,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
           }
         }
       }
-#endif
+#endif  // DECDEC_ROW_STEP
+#endif  // DECDEC_SKIP_COMPUTE
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done reading the stage
       int nrows = 0;

@@ -12,15 +12,15 @@ using namespace decdec;
 
 __global__ void k_sel(const uint16_t* x, int n, int q, int iters, int* idx, uint16_t* xs, unsigned long long* tr) {
   extern __shared__ __align__(16) uint8_t smem[];
-  SelectSmemR* S = reinterpret_cast<SelectSmemR*>(smem);
-  int* sidx = reinterpret_cast<int*>(smem + sizeof(SelectSmemR));
+  SelectSmemS* S = reinterpret_cast<SelectSmemS*>(smem);
+  int* sidx = reinterpret_cast<int*>(smem + select_split_smem_bytes(n));
   uint16_t* sxs = reinterpret_cast<uint16_t*>(sidx + q);
-  select_regs_zero(S);
-  __syncthreads();
   for (int it = 0; it < iters; ++it) {
+    select_split_zero(S, n);
+    __syncthreads();
     unsigned long long* t = tr + it * 20;
     if (threadIdx.x == 0) t[15] = clock64();
-    select_block_regs_any(x, n, q, 0, sidx, sxs, nullptr, S, t);
+    select_split_any(x, n, q, sidx, sxs, nullptr, S, (blockDim.x >> 5) - 1, t);
     __syncthreads();
     if (threadIdx.x == 0) t[14] = clock64();
   }
@@ -42,7 +42,7 @@ int main() {
       const int iters = getenv("ITERS") ? atoi(getenv("ITERS")) : 20;
       CK(cudaMalloc(&dx, n * 2)); CK(cudaMalloc(&didx, q * 4)); CK(cudaMalloc(&dxs, q * 2)); CK(cudaMalloc(&dtr, iters * 20 * 8));
       CK(cudaMemcpy(dx, hx, n * 2, cudaMemcpyHostToDevice));
-      const size_t sm = sizeof(SelectSmemR) + q * 6 + 64;
+      const size_t sm = select_split_smem_bytes(n) + q * 6 + 64;
       CK(cudaFuncSetAttribute(k_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       k_sel<<<1, nt, sm>>>(dx, n, q, iters, didx, dxs, dtr);
       CK(cudaDeviceSynchronize());
@@ -50,9 +50,9 @@ int main() {
       CK(cudaMemcpy(h, dtr, iters * 20 * 8, cudaMemcpyDeviceToHost));
       for (int it : {0, 1, iters - 1}) {
         unsigned long long* t = h + it * 20;
-        printf("{\"n\": %d, \"threads\": %d, \"iter\": %d, \"cycles\": [%lld, %lld, %lld, %lld, %lld]}\n", n, nt, it,
-               (long long)(t[16] - t[15]), (long long)(t[17] - t[15]), (long long)(t[18] - t[15]), (long long)(t[19] - t[15]),
-               (long long)(t[14] - t[15]));
+        printf("{\"n\": %d, \"threads\": %d, \"iter\": %d, \"cycles (loads, coarse, D placed, T found, R placed, published, all)\": [%lld, %lld, %lld, %lld, %lld, %lld, %lld]}\n", n, nt, it,
+               (long long)(t[16] - t[15]), (long long)(t[17] - t[15]), (long long)(t[18] - t[15]), (long long)(t[11] - t[15]),
+               (long long)(t[13] - t[15]), (long long)(t[19] - t[15]), (long long)(t[14] - t[15]));
       }
     }
   }

@@ -401,6 +401,221 @@ __device__ __forceinline__ void select_block_regs(const uint16_t* __restrict__ x
 #undef SEL_TRACE
 }
 
+
+// ---------------------------------------------------------------- DEC CTA variant (split order)
+// Same selected set as select_block, placed in a different (still deterministic) order that
+// lets the caller start gathering before the selection finishes:
+//   positions [0, D)  : keys whose coarse bin (key >> 7) is above the threshold bin, ascending
+//                       index -- known after the first histogram (three block barriers);
+//   positions [D, q)  : the rest R (threshold bin: key > T, then the lowest-index ties),
+//                       ascending -- written by ONE finisher warp from a bitmap of the
+//                       threshold-bin candidates, published through a shared flag (no block
+//                       barrier, so the other warps' gathers of [0, D) are already in flight).
+// Returns D.  The caller's warps may use positions < D immediately; positions >= D after
+// select_wait_rest().  If sel_out is non-null the finisher also writes the whole selection
+// in ascending index order (merge of the two sorted runs; the decdec_linear `sel` contract).
+struct SelectSmemS {
+  SelectSmemR r;
+  uint32_t bitmap[1024];  // threshold-bin candidates, bit i = key i (n <= 32768)
+  uint32_t rest_ready;
+  uint32_t pad[3];
+  // followed by the staged keys: uint16_t [n] (select_split_smem_bytes)
+};
+__host__ __device__ inline size_t select_split_smem_bytes(int n) { return sizeof(SelectSmemS) + (size_t)((n + 7) / 8) * 16; }
+__device__ __forceinline__ void select_split_zero(SelectSmemS* S, int n) {
+  select_regs_zero(&S->r);
+  for (int i = threadIdx.x; i < (n + 31) / 32; i += blockDim.x) S->bitmap[i] = 0u;
+  if (threadIdx.x == 0) S->rest_ready = 0u;
+}
+__device__ __forceinline__ void select_wait_rest(const SelectSmemS* S) {
+  while (*reinterpret_cast<const volatile uint32_t*>(&S->rest_ready) == 0u) {
+  }
+  __threadfence_block();
+}
+
+template <int MAXC>
+__device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int n, int q, int* __restrict__ idx_out,
+                                            uint16_t* __restrict__ xs_out, int* __restrict__ sel_out, SelectSmemS* SS,
+                                            int finisher, unsigned long long* tr) {
+#define SEL_TRACE(i)                                  \
+  do {                                                \
+    if (tr && threadIdx.x == 0) tr[i] = clock64();     \
+  } while (0)
+  SelectSmemR* S = &SS->r;
+  const int t = threadIdx.x, NT = blockDim.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
+  const int n8 = n >> 3;
+  const int C = (n8 + NT - 1) / NT;  // <= MAXC (caller's guarantee)
+  const int c0 = t * C;
+  const int nv = max(0, min(C, n8 - c0));
+  uint4 v[MAXC];
+  const uint4* x4 = reinterpret_cast<const uint4*>(x) + c0;
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) v[m] = m < nv ? __ldg(x4 + m) : make_uint4(0, 0, 0, 0);
+  SEL_TRACE(16);
+  uint4* sx = reinterpret_cast<uint4*>(SS + 1);  // staged keys for the finisher warp
+  // ---- coarse histogram (key >> 7), 4 copies
+  uint32_t* hA = S->histA[lane & 3];
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) {
+    if (m < nv) {
+      sx[c0 + m] = v[m];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t b = (chunk_elem(v[m], j) & 0x7fffu) >> 7;
+        atomicAdd(&hA[b + (b >> 3)], 1u);
+      }
+    }
+  }
+  __syncthreads();  // barrier 1
+  uint32_t bA, nD;
+  {
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      c[j] = S->histA[0][9 * lane + j] + S->histA[1][9 * lane + j] + S->histA[2][9 * lane + j] + S->histA[3][9 * lane + j];
+    warp_find_bin_all<8>(c, (uint32_t)q, &bA, &nD);
+  }
+  SEL_TRACE(17);
+  // ---- D counts; fine histogram + candidate bitmap of bin bA
+  uint32_t n_d = 0;
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) {
+    if (m < nv) {
+      uint32_t bits = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t key = chunk_elem(v[m], j) & 0x7fffu;
+        const uint32_t b = key >> 7;
+        n_d += b > bA;
+        if (b == bA) {
+          const uint32_t fb = key & 127u;
+          atomicAdd(&S->histB[fb + (fb >> 2)], 1u);
+          bits |= 1u << j;
+        }
+      }
+      if (bits) atomicOr(&SS->bitmap[(c0 + m) >> 2], bits << (8 * ((c0 + m) & 3)));
+    }
+  }
+  uint32_t inc_d = n_d;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc_d, o);
+    if (lane >= o) inc_d += u;
+  }
+  if (lane == 31) S->wsum[wid] = inc_d;
+  __syncthreads();  // barrier 2: histB, bitmap, D warp totals complete
+  uint32_t pre_d;
+  {
+    const uint32_t wt = lane < nw ? S->wsum[lane] : 0u;
+    uint32_t wi = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    pre_d = __shfl_sync(0xffffffffu, wi - wt, wid) + inc_d - n_d;
+  }
+  if (n_d) {  // place D at [0, nD), ascending
+    int pos = (int)pre_d;
+#pragma unroll
+    for (int m = 0; m < MAXC; ++m) {
+      if (m < nv) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t raw = chunk_elem(v[m], j);
+          if (((raw & 0x7fffu) >> 7) > bA) {
+            idx_out[pos] = 8 * (c0 + m) + j;
+            xs_out[pos] = (uint16_t)raw;
+            ++pos;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();  // barrier 3: D placed
+  SEL_TRACE(18);
+  if (wid == finisher) {
+    // ---- threshold T inside bin bA, then R from the bitmap in index order
+    uint32_t T, need;
+    {
+      uint32_t c[4], bin, above;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[j] = S->histB[5 * lane + j];
+      warp_find_bin_all<4>(c, (uint32_t)q - nD, &bin, &above);
+      T = (bA << 7) | bin;
+      need = (uint32_t)q - nD - above;
+    }
+    if (tr && lane == 0) tr[11] = clock64();
+    const int nwords = (n + 31) >> 5;
+    const int W = (nwords + 31) >> 5;  // lane l owns bitmap words [l*W, l*W + W): index order
+    const int w_lo = min(lane * W, nwords), w_hi = min(w_lo + W, nwords);
+    const uint16_t* xk = reinterpret_cast<const uint16_t*>(sx);
+    uint32_t n_gt = 0, n_eq = 0;  // pass 1: counts of key > T / key == T among my candidates
+    for (int w = w_lo; w < w_hi; ++w) {
+      for (uint32_t bb = SS->bitmap[w]; bb; bb &= bb - 1) {
+        const uint32_t key = xk[32 * w + __ffs(bb) - 1] & 0x7fffu;
+        n_gt += key > T;
+        n_eq += key == T;
+      }
+    }
+    uint32_t inc = (n_eq << 16) | n_gt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    const uint32_t pre = inc - ((n_eq << 16) | n_gt);
+    uint32_t eq_seen = pre >> 16, g_seen = pre & 0xffffu;
+    if (n_gt + n_eq) {  // pass 2: write my taken candidates at nD + (#taken before them)
+      for (int w = w_lo; w < w_hi; ++w) {
+        for (uint32_t bb = SS->bitmap[w]; bb; bb &= bb - 1) {
+          const int i = 32 * w + __ffs(bb) - 1;
+          const uint16_t raw = xk[i];
+          const uint32_t key = raw & 0x7fffu;
+          if (key > T) {
+            const uint32_t pos = nD + g_seen + min(eq_seen, need);
+            idx_out[pos] = i;
+            xs_out[pos] = raw;
+            ++g_seen;
+          } else if (key == T) {
+            if (eq_seen < need) {
+              const uint32_t pos = nD + g_seen + eq_seen;
+              idx_out[pos] = i;
+              xs_out[pos] = raw;
+            }
+            ++eq_seen;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (tr && lane == 0) tr[13] = clock64();
+    if (sel_out) {  // merge the two ascending runs [0, nD) and [nD, q) into sel_out
+      const int nR = q - (int)nD;
+      for (int a = lane; a < (int)nD; a += 32) {  // D element: + #R below it
+        const int v0 = idx_out[a];
+        int lo = 0, hi = nR;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (idx_out[nD + mid] < v0) lo = mid + 1; else hi = mid; }
+        sel_out[a + lo] = v0;
+      }
+      for (int r = lane; r < nR; r += 32) {  // R element: + #D below it
+        const int v0 = idx_out[nD + r];
+        int lo = 0, hi = (int)nD;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (idx_out[mid] < v0) lo = mid + 1; else hi = mid; }
+        sel_out[r + lo] = v0;
+      }
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) {
+      *reinterpret_cast<volatile uint32_t*>(&SS->rest_ready) = 1u;
+      if (tr) tr[19] = clock64();
+    }
+  }
+  return (int)nD;
+#undef SEL_TRACE
+}
+
 // Dispatch on the chunks per thread (fewer unrolled slots -> less predication overhead).
 __device__ __forceinline__ bool select_block_regs_any(const uint16_t* x, int n, int q, int idx_base, int* idx_out,
                                                       uint16_t* xs_out, int* sel_out, SelectSmemR* S,
@@ -412,6 +627,18 @@ __device__ __forceinline__ bool select_block_regs_any(const uint16_t* x, int n, 
   else if (C <= 8) select_block_regs<8>(x, n, q, idx_base, idx_out, xs_out, sel_out, S, tr);
   else return false;
   return true;
+}
+
+// Returns D (>= 0), or -1 if the segment does not fit in registers (caller falls back).
+__device__ __forceinline__ int select_split_any(const uint16_t* x, int n, int q, int* idx_out, uint16_t* xs_out,
+                                                int* sel_out, SelectSmemS* S, int finisher, unsigned long long* tr) {
+  const int C = ((n >> 3) + (int)blockDim.x - 1) / (int)blockDim.x;
+  if (n > 32 * 1024) return -1;
+  if (C <= 1) return select_split<1>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
+  if (C <= 2) return select_split<2>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
+  if (C <= 4) return select_split<4>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
+  if (C <= 8) return select_split<8>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
+  return -1;
 }
 
 // Standalone selector (decdec_select): one block per segment.
