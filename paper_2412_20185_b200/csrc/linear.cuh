@@ -117,7 +117,11 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   const int seg_len = p.chunk ? min(p.chunk, p.d_in) : p.d_in;
   const bool regs = (seg_len / 8 + (int)blockDim.x - 1) / (int)blockDim.x <= kSelRegChunks;
   const bool split = !p.chunk && regs && p.d_in <= 32 * 1024;
+#ifndef DECDEC_SPLIT_BARRIER
   if (split) select_split_zero(SS, p.d_in);  // before the wait: smem is ours already
+#else
+  if (split) select_regs_zero(SR);
+#endif
   else if (regs) select_regs_zero(SR);
   __syncthreads();
   pdl_wait();  // x may be the previous layer's product; the workspace is the previous layer's
@@ -185,8 +189,23 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   // rows whose coarse bin is above the threshold bin (positions [0, nD)) are known after three
   // block barriers; the last warp finishes the rest alone while the others start gathering.
   int nD = -1;
+  bool issued = false;
   if (split) {
+#ifndef DECDEC_SPLIT_BARRIER
     nD = select_split_any(p.x, p.d_in, p.k_req, sidx, sxs, blockIdx.x == 0 ? p.sel_out : nullptr, SS, nw - 1, tr);
+#else
+    auto early = [&](int n_def) {  // cp.async only: the remaining block barriers do not wait for it
+      if (it < n_items && min((it / ns) * p.rpi + p.rpi, p.k_sel) <= n_def) {
+        issue(it, 0);
+        issued = true;
+      }
+    };
+    nD = select_split_bar_any(p.x, p.d_in, p.k_req, sidx, sxs, blockIdx.x == 0 ? p.sel_out : nullptr, SR, tr, early);
+    if (nD >= 0) {
+      __syncthreads();  // R placed
+      nD = p.k_sel;
+    }
+#endif
 #ifdef DECDEC_SPLIT_SERIAL
     __syncthreads();  // experiment switch: wait for the finisher before any gather
     if (nD >= 0) nD = p.k_sel;
@@ -220,7 +239,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     if (tr) tr[14] = clock64();
   }
   // ---- steps 2-3: gather rows S of R_hat x x[S] for this CTA's segments (double-buffered)
-  if (it < n_items) {
+  if (it < n_items && !issued) {
     ready(it);
     issue(it, 0);
   }

@@ -53,6 +53,7 @@ int main() {
         printf("{\"n\": %d, \"threads\": %d, \"iter\": %d, \"cycles (loads, coarse, D placed, T found, R placed, published, all)\": [%lld, %lld, %lld, %lld, %lld, %lld, %lld]}\n", n, nt, it,
                (long long)(t[16] - t[15]), (long long)(t[17] - t[15]), (long long)(t[18] - t[15]), (long long)(t[11] - t[15]),
                (long long)(t[13] - t[15]), (long long)(t[19] - t[15]), (long long)(t[14] - t[15]));
+        printf("   finisher: pass1 done %lld, scan done %lld\n", (long long)(t[1] - t[15]), (long long)(t[2] - t[15]));
       }
     }
   }

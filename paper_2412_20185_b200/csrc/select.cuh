@@ -414,22 +414,27 @@ __device__ __forceinline__ void select_block_regs(const uint16_t* __restrict__ x
 // Returns D.  The caller's warps may use positions < D immediately; positions >= D after
 // select_wait_rest().  If sel_out is non-null the finisher also writes the whole selection
 // in ascending index order (merge of the two sorted runs; the decdec_linear `sel` contract).
+constexpr int kCandList = 64;  // threshold-bin candidates kept as a sortable list (else bitmap scan)
 struct SelectSmemS {
   SelectSmemR r;
   uint32_t bitmap[1024];  // threshold-bin candidates, bit i = key i (n <= 32768)
+  uint32_t cand[kCandList];  // (index << 15 | key) of threshold-bin candidates, arrival order
   uint32_t rest_ready;
-  uint32_t pad[3];
+  uint32_t ncand;
+  uint32_t pad[2];
   // followed by the staged keys: uint16_t [n] (select_split_smem_bytes)
 };
 __host__ __device__ inline size_t select_split_smem_bytes(int n) { return sizeof(SelectSmemS) + (size_t)((n + 7) / 8) * 16; }
 __device__ __forceinline__ void select_split_zero(SelectSmemS* S, int n) {
   select_regs_zero(&S->r);
   for (int i = threadIdx.x; i < (n + 31) / 32; i += blockDim.x) S->bitmap[i] = 0u;
-  if (threadIdx.x == 0) S->rest_ready = 0u;
+  if (threadIdx.x == 0) {
+    S->rest_ready = 0u;
+    S->ncand = 0u;
+  }
 }
 __device__ __forceinline__ void select_wait_rest(const SelectSmemS* S) {
-  while (*reinterpret_cast<const volatile uint32_t*>(&S->rest_ready) == 0u) {
-  }
+  while (*reinterpret_cast<const volatile uint32_t*>(&S->rest_ready) == 0u) __nanosleep(100);  // keep the LSU free
   __threadfence_block();
 }
 
@@ -476,24 +481,33 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
     warp_find_bin_all<8>(c, (uint32_t)q, &bA, &nD);
   }
   SEL_TRACE(17);
-  // ---- D counts; fine histogram + candidate bitmap of bin bA
-  uint32_t n_d = 0;
+  // ---- D counts; fine histogram + candidate bitmap/list of bin bA.  Per chunk the per-key
+  // work is branch-free (masks); the rare keys in bin bA take one branch per chunk.
+  uint32_t n_d = 0, dmask[MAXC];
 #pragma unroll
   for (int m = 0; m < MAXC; ++m) {
+    dmask[m] = 0;
     if (m < nv) {
       uint32_t bits = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const uint32_t key = chunk_elem(v[m], j) & 0x7fffu;
-        const uint32_t b = key >> 7;
-        n_d += b > bA;
-        if (b == bA) {
+        const uint32_t b = (chunk_elem(v[m], j) & 0x7fffu) >> 7;
+        dmask[m] |= (uint32_t)(b > bA) << j;
+        bits |= (uint32_t)(b == bA) << j;
+      }
+      n_d += __popc(dmask[m]);
+      if (bits) {
+        atomicOr(&SS->bitmap[(c0 + m) >> 2], bits << (8 * ((c0 + m) & 3)));
+        const uint32_t slot = atomicAdd(&SS->ncand, (uint32_t)__popc(bits));
+        uint32_t o = slot;
+        for (uint32_t bb = bits; bb; bb &= bb - 1, ++o) {
+          const int jj = __ffs(bb) - 1;
+          const uint32_t key = chunk_elem(v[m], jj) & 0x7fffu;
           const uint32_t fb = key & 127u;
           atomicAdd(&S->histB[fb + (fb >> 2)], 1u);
-          bits |= 1u << j;
+          if (o < (uint32_t)kCandList) SS->cand[o] = ((uint32_t)(8 * (c0 + m) + jj) << 15) | key;
         }
       }
-      if (bits) atomicOr(&SS->bitmap[(c0 + m) >> 2], bits << (8 * ((c0 + m) & 3)));
     }
   }
   uint32_t inc_d = n_d;
@@ -515,20 +529,15 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
     }
     pre_d = __shfl_sync(0xffffffffu, wi - wt, wid) + inc_d - n_d;
   }
-  if (n_d) {  // place D at [0, nD), ascending
+  if (n_d) {  // place D at [0, nD), ascending (only the few threads holding D keys)
     int pos = (int)pre_d;
 #pragma unroll
     for (int m = 0; m < MAXC; ++m) {
-      if (m < nv) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t raw = chunk_elem(v[m], j);
-          if (((raw & 0x7fffu) >> 7) > bA) {
-            idx_out[pos] = 8 * (c0 + m) + j;
-            xs_out[pos] = (uint16_t)raw;
-            ++pos;
-          }
-        }
+      for (uint32_t bb = dmask[m]; bb; bb &= bb - 1) {
+        const int jj = __ffs(bb) - 1;
+        idx_out[pos] = 8 * (c0 + m) + jj;
+        xs_out[pos] = (uint16_t)chunk_elem(v[m], jj);
+        ++pos;
       }
     }
   }
@@ -546,6 +555,55 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
       need = (uint32_t)q - nD - above;
     }
     if (tr && lane == 0) tr[11] = clock64();
+    const uint32_t ncand = SS->ncand;
+    if (ncand <= (uint32_t)kCandList) {
+      // sort the candidates by index (bitonic over 64 = 2 per lane, keys ride in the low bits)
+      uint32_t e0 = lane < (int)ncand ? SS->cand[lane] : 0xffffffffu;
+      uint32_t e1 = lane + 32 < (int)ncand ? SS->cand[lane + 32] : 0xffffffffu;
+#pragma unroll
+      for (int k2 = 2; k2 <= 64; k2 <<= 1) {
+#pragma unroll
+        for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+          if (j2 == 32) {  // partner in the other half, same lane
+            const bool up = ((lane & k2) == 0);  // k2 == 64: always ascending
+            const uint32_t lo = min(e0, e1), hi = max(e0, e1);
+            e0 = up ? lo : hi;
+            e1 = up ? hi : lo;
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int pos = lane + 32 * h;
+              uint32_t& e = h ? e1 : e0;
+              const uint32_t o = __shfl_xor_sync(0xffffffffu, e, j2);
+              const bool up = ((pos & k2) == 0);
+              const bool lower = (pos & j2) == 0;
+              e = (lower == up) ? min(e, o) : max(e, o);
+            }
+          }
+        }
+      }
+      // positions in index order: taken = key > T, or key == T among the first `need` ties
+      const uint32_t lt = (1u << lane) - 1u;
+      uint32_t taken_before = 0, eq_before = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t e = h ? e1 : e0;
+        const bool valid = e != 0xffffffffu;
+        const uint32_t key = e & 0x7fffu;
+        const bool gt = valid && key > T, eq = valid && key == T;
+        const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+        const uint32_t my_eq = eq_before + __popc(beq & lt);
+        const bool take = gt || (eq && my_eq < need);
+        const uint32_t bt = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const uint32_t pos = nD + taken_before + __popc(bt & lt);
+          idx_out[pos] = (int)(e >> 15);
+          xs_out[pos] = x[e >> 15];
+        }
+        taken_before += __popc(bt);
+        eq_before += __popc(beq);
+      }
+    } else {
     const int nwords = (n + 31) >> 5;
     const int W = (nwords + 31) >> 5;  // lane l owns bitmap words [l*W, l*W + W): index order
     const int w_lo = min(lane * W, nwords), w_hi = min(w_lo + W, nwords);
@@ -558,6 +616,9 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
         n_eq += key == T;
       }
     }
+#ifdef DECDEC_FINISHER_TRACE
+    if (tr && lane == 0) tr[1] = clock64();
+#endif
     uint32_t inc = (n_eq << 16) | n_gt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -565,6 +626,9 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
       if (lane >= o) inc += u;
     }
     const uint32_t pre = inc - ((n_eq << 16) | n_gt);
+#ifdef DECDEC_FINISHER_TRACE
+    if (tr && lane == 0) tr[2] = clock64();
+#endif
     uint32_t eq_seen = pre >> 16, g_seen = pre & 0xffffu;
     if (n_gt + n_eq) {  // pass 2: write my taken candidates at nD + (#taken before them)
       for (int w = w_lo; w < w_hi; ++w) {
@@ -588,6 +652,7 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
         }
       }
     }
+    }  // bitmap path
     __syncwarp();
     if (tr && lane == 0) tr[13] = clock64();
     if (sel_out) {  // merge the two ascending runs [0, nD) and [nD, q) into sel_out
@@ -638,6 +703,198 @@ __device__ __forceinline__ int select_split_any(const uint16_t* x, int n, int q,
   if (C <= 2) return select_split<2>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
   if (C <= 4) return select_split<4>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
   if (C <= 8) return select_split<8>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
+  return -1;
+}
+
+
+// Block-barrier variant of the split order (same positions as select_split): after D is placed
+// every thread calls early(D) -- which must only issue cp.async (no register destinations:
+// a block barrier would wait for those) -- then all threads place R with one more block scan.
+// Four block barriers; sel_out (if non-null) in ascending order.
+template <int MAXC, typename Early>
+__device__ __forceinline__ int select_split_bar(const uint16_t* __restrict__ x, int n, int q, int* __restrict__ idx_out,
+                                                uint16_t* __restrict__ xs_out, int* __restrict__ sel_out,
+                                                SelectSmemR* S, unsigned long long* tr, Early&& early) {
+#define SEL_TRACE(i)                                  \
+  do {                                                \
+    if (tr && threadIdx.x == 0) tr[i] = clock64();     \
+  } while (0)
+  const int t = threadIdx.x, NT = blockDim.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
+  const int n8 = n >> 3;
+  const int C = (n8 + NT - 1) / NT;
+  const int c0 = t * C;
+  const int nv = max(0, min(C, n8 - c0));
+  uint4 v[MAXC];
+  const uint4* x4 = reinterpret_cast<const uint4*>(x) + c0;
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) v[m] = m < nv ? __ldg(x4 + m) : make_uint4(0, 0, 0, 0);
+  SEL_TRACE(16);
+  uint32_t* hA = S->histA[lane & 3];
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) {
+    if (m < nv) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t b = (chunk_elem(v[m], j) & 0x7fffu) >> 7;
+        atomicAdd(&hA[b + (b >> 3)], 1u);
+      }
+    }
+  }
+  __syncthreads();  // barrier 1
+  uint32_t bA, nD;
+  {
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      c[j] = S->histA[0][9 * lane + j] + S->histA[1][9 * lane + j] + S->histA[2][9 * lane + j] + S->histA[3][9 * lane + j];
+    warp_find_bin_all<8>(c, (uint32_t)q, &bA, &nD);
+  }
+  SEL_TRACE(17);
+  uint32_t n_d = 0;
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) {
+    if (m < nv) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t key = chunk_elem(v[m], j) & 0x7fffu;
+        const uint32_t b = key >> 7;
+        n_d += b > bA;
+        if (b == bA) {
+          const uint32_t fb = key & 127u;
+          atomicAdd(&S->histB[fb + (fb >> 2)], 1u);
+        }
+      }
+    }
+  }
+  uint32_t inc_d = n_d;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc_d, o);
+    if (lane >= o) inc_d += u;
+  }
+  if (lane == 31) S->wsum[wid] = inc_d;
+  __syncthreads();  // barrier 2: histB complete, D warp totals visible
+  uint32_t pre_d;
+  {
+    const uint32_t wt = lane < nw ? S->wsum[lane] : 0u;
+    uint32_t wi = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    pre_d = __shfl_sync(0xffffffffu, wi - wt, wid) + inc_d - n_d;
+  }
+  if (n_d) {
+    int pos = (int)pre_d;
+#pragma unroll
+    for (int m = 0; m < MAXC; ++m) {
+      if (m < nv) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t raw = chunk_elem(v[m], j);
+          if (((raw & 0x7fffu) >> 7) > bA) {
+            idx_out[pos] = 8 * (c0 + m) + j;
+            xs_out[pos] = (uint16_t)raw;
+            ++pos;
+          }
+        }
+      }
+    }
+  }
+  uint32_t T, need_u;
+  {
+    uint32_t c[4], bin, above;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[j] = S->histB[5 * lane + j];
+    warp_find_bin_all<4>(c, (uint32_t)q - nD, &bin, &above);
+    T = (bA << 7) | bin;
+    need_u = (uint32_t)q - nD - above;
+  }
+  const int need = (int)need_u;
+  uint32_t n_g = 0, n_eq = 0;
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) {
+    if (m < nv) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t key = chunk_elem(v[m], j) & 0x7fffu;
+        n_g += (key >> 7) == bA && key > T;
+        n_eq += key == T;
+      }
+    }
+  }
+  const uint32_t mine = (n_eq << 16) | n_g;
+  uint32_t inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  __syncthreads();  // barrier 3: D placed; wsum (D) and histB read by every warp
+  SEL_TRACE(18);
+  early((int)nD);
+  if (lane == 31) S->wsum[wid] = inc;
+  __syncthreads();  // barrier 4: R warp totals visible
+  uint32_t wpre;
+  {
+    const uint32_t wt = lane < nw ? S->wsum[lane] : 0u;
+    uint32_t wi = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    wpre = __shfl_sync(0xffffffffu, wi - wt, wid);
+  }
+  SEL_TRACE(19);
+  const uint32_t pre = wpre + inc - mine;
+  if (n_g + n_eq || (sel_out && n_d)) {
+    int eq_seen = (int)(pre >> 16);
+    int g_seen = (int)(pre & 0xffffu);
+    int d_seen = (int)pre_d;
+#pragma unroll
+    for (int m = 0; m < MAXC; ++m) {
+      if (m < nv) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t raw = chunk_elem(v[m], j);
+          const uint32_t key = raw & 0x7fffu;
+          const int i = 8 * (c0 + m) + j;
+          const uint32_t b = key >> 7;
+          if (b > bA) {
+            if (sel_out) sel_out[d_seen + g_seen + min(eq_seen, need)] = i;
+            ++d_seen;
+          } else if (b == bA && key > T) {
+            const int r = (int)nD + g_seen + min(eq_seen, need);
+            idx_out[r] = i;
+            xs_out[r] = (uint16_t)raw;
+            if (sel_out) sel_out[d_seen + g_seen + min(eq_seen, need)] = i;
+            ++g_seen;
+          } else if (key == T) {
+            if (eq_seen < need) {
+              idx_out[(int)nD + g_seen + eq_seen] = i;
+              xs_out[(int)nD + g_seen + eq_seen] = (uint16_t)raw;
+              if (sel_out) sel_out[d_seen + g_seen + eq_seen] = i;
+            }
+            ++eq_seen;
+          }
+        }
+      }
+    }
+  }
+  return (int)nD;
+#undef SEL_TRACE
+}
+
+template <typename Early>
+__device__ __forceinline__ int select_split_bar_any(const uint16_t* x, int n, int q, int* idx_out, uint16_t* xs_out,
+                                                    int* sel_out, SelectSmemR* S, unsigned long long* tr, Early&& early) {
+  const int C = ((n >> 3) + (int)blockDim.x - 1) / (int)blockDim.x;
+  if (C <= 1) return select_split_bar<1>(x, n, q, idx_out, xs_out, sel_out, S, tr, early);
+  if (C <= 2) return select_split_bar<2>(x, n, q, idx_out, xs_out, sel_out, S, tr, early);
+  if (C <= 4) return select_split_bar<4>(x, n, q, idx_out, xs_out, sel_out, S, tr, early);
+  if (C <= 8) return select_split_bar<8>(x, n, q, idx_out, xs_out, sel_out, S, tr, early);
   return -1;
 }
 

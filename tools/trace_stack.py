@@ -93,6 +93,13 @@ for i, (b, name, d_in, d_out) in enumerate(meta):
 nl = len(meta) // a.blocks
 if a.blocks > 1:
     print(f"last block: {(ends[-1] - ends[-1 - nl]) / 1e3:.2f} us (end to end)")
+print("DEC CTAs (µs, median / max over DEC CTAs): sel_start, D placed (warp 0), gather done warp 0, last warp, all partials, combine done")
+for i, (b, name, d_in, d_out) in enumerate(meta):
+    ev = ev_all[i]
+    dec = ev[(ev[:, 5] > 0) & (ev[:, 8] == 0)]
+    if len(dec):
+        cols = [5, 6, 7, 1, 12, 9]
+        print(f"  {b}:{name:4s}", " | ".join(f"{med(dec[:, c]):7.2f} {mx(dec[:, c]):7.2f}" for c in cols))
 rows = []
 for i, (b, name, d_in, d_out) in enumerate(meta):
     ev = ev_all[i]
