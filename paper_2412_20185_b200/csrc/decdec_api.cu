@@ -46,8 +46,9 @@ constexpr size_t kSmemBudget = 200 * 1024;
 // Launch plan: enumerate (consumer warps NC, rows per slot RPS); pick the one minimising the
 // busiest CTA's bytes (ceil(tiles / SMs) x (stage bytes + a per-tile overhead equivalent)),
 // ties -> more consumer warps.  DECDEC_PLAN="NC,RPS" overrides (tuning).
-// Number of DEC CTAs: ~272 warps of zero-copy loads (measured on the llama3-8b stack at
-// k_chunk 21: 16 DEC CTAs of 17 warps beat 8 by 6%, 4 by 21%); DECDEC_NDEC overrides.
+// Number of DEC CTAs: ~544 warps of zero-copy reads (measured on the llama3-8b stack at
+// k_chunk 21, 17-warp CTAs: 4 -> 105 us/block, 8 -> 92, 16 -> 84, 32 -> 80, 64 -> 78 within
+// noise, while the GEMV CTAs lose SMs); DECDEC_NDEC overrides.
 int dec_ctas(int warps_per_cta) {
   static int env = -1;
   if (env < 0) {
@@ -55,8 +56,8 @@ int dec_ctas(int warps_per_cta) {
     env = e ? atoi(e) : 0;
   }
   if (env > 0) return env;
-  int n = (272 + warps_per_cta - 1) / warps_per_cta;
-  return n < 2 ? 2 : (n > 16 ? 16 : n);
+  int n = (544 + warps_per_cta - 1) / warps_per_cta;
+  return n < 2 ? 2 : (n > 32 ? 32 : n);
 }
 
 // DEC CTA layout: CTA c owns segments c, c + n_dec, ...; a segment's k_sel rows are split in
@@ -161,7 +162,8 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
       if (p.smem > kSmemBudget + 16 * 1024) continue;
       const double waves = (double)((p.n_tiles + max_grid - 1) / max_grid);
       // more consumer warps hide more latency (measured: 16 warps beat 8 by 6-11% on the big layers)
-      const double cost = waves * ((double)p.stage_bytes + 8192.0) * (1.0 + 2.0 / nc) * (rps == 1 ? 1.5 : 1.0);
+      double cost = waves * ((double)p.stage_bytes + 8192.0) * (1.0 + 2.0 / nc) * (rps == 1 ? 1.5 : 1.0);
+      if (k_sel > 0) cost *= 1.0 + 0.5 * (16 - nc) / 16.0;  // DEC CTAs gather with every warp of the CTA
       if (!have || cost < best_cost * 0.999 || (cost <= best_cost * 1.001 && p.NC > best.NC)) {
         best = p;
         best_cost = cost;
