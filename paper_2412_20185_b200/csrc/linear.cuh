@@ -613,6 +613,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       for (int tile = cta; tile < p.n_tiles; tile += n_cta)
         gemv_publish(p, (tile * TR) / kSegCols, (uint32_t)nrows_tile, lane);
     }
+    if (ct == 0) DECDEC_TRACE(p, 10);  // o_b published (this warp)
     return;
   }
 }

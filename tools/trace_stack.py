@@ -84,10 +84,10 @@ for i, (b, name, d_in, d_out) in enumerate(meta):
     end = ev[:, :E].max()
     ends.append(end)
     nxt = mn(ev_all[i + 1][:, 8]) if i + 1 < len(meta) else float("nan")
-    line = f"{b}:{name:4s} start {mn(ev[:, 0]):8.2f} | rel {mn(gem[:, 8]):8.2f} x {med(gem[:, 2]):8.2f} gemv {mx(gem[:, 4]):8.2f}"
+    line = f"{b}:{name:4s} start {mn(ev[:, 0]):8.2f} | rel {mn(gem[:, 8]):8.2f} x {med(gem[:, 2]):8.2f} gemv {mx(gem[:, 4]):8.2f} pub {mx(gem[:, 10]):8.2f}"
     if len(dec):
         line += (f" | sel {med(dec[:, 5]):8.2f} -> {mx(dec[:, 6]):8.2f} gath {mx(np.maximum(dec[:, 7], dec[:, 1])):8.2f}"
-                 f" arr {mx(dec[:, 13]):8.2f} comb {mx(dec[:, 9]):8.2f}")
+                 f" comb {mx(dec[:, 9]):8.2f}")
     line += f" | end {us(end):8.2f} next {nxt:8.2f}"
     print(line)
 nl = len(meta) // a.blocks
