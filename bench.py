@@ -288,6 +288,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nx", type=int, default=4, help="distinct activation sets cycled across steps")
     ap.add_argument("--quick", action="store_true", help="headline step only (for ncu launch lists)")
+    ap.add_argument("--sweep-only", action="store_true", help="decode-step sweep only (no per-shape table, no oracle)")
     ap.add_argument("--unfused", action="store_true",
                     help="7 separate q/k/v/o/gate/up/down calls per block instead of the paper's layer "
                          "classes qkv, o, gu, d (P:304); per-layer µs of the 7 shapes are reported either way")
@@ -317,6 +318,8 @@ def main():
     sweep = sorted({int(v) for v in args.sweep.split(",") if v != ""} | {args.kchunk})
     if args.quick:
         sweep, args.no_cpu_baseline = [args.kchunk], True
+    if args.sweep_only:
+        args.no_cpu_baseline = True
     max_k = k_of(max(sweep), M.max_d_in)
     ws = dd.Workspace(max_k, M.max_d_out)
     torch.cuda.synchronize()
@@ -371,7 +374,7 @@ def main():
         if name not in shape_names:
             shape_names.append(name)
     per_shape = {}
-    if world == 1 and not args.quick:
+    if world == 1 and not (args.quick or args.sweep_only):
         for name in shape_names:
             idx = [i for i, m in enumerate(M.meta) if m[1] == name]
             d_in, d_out = M.meta[idx[0]][2], M.meta[idx[0]][3]
@@ -394,7 +397,7 @@ def main():
 
     # ---- e2e through the public API: H2D inputs + step + D2H outputs ------------------------
     e2e = None
-    if world == 1 and not args.quick:
+    if world == 1 and not (args.quick or args.sweep_only):
         x_pinned = [torch.from_numpy(h).pin_memory() for h in M.x_host]
         y_pinned = torch.empty(M.y_dev.numel(), dtype=torch.float16).pin_memory()
         stack = dd.Stack(M.layers, M.ks(args.kchunk), M.xs(0), M.ys(), ws)

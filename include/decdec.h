@@ -85,13 +85,18 @@ typedef struct decdec_layer {
   const uint16_t* r_scales;  /* HOST mapped fp16 [d_out] (r_bits = 4) | NULL (r_bits = 16) */
 } decdec_layer;
 
-/* Bytes of workspace for layers with k <= max_k and d_out <= max_d_out: the fp32 base
- * output o_b (d_out) and per-256-column arrival counters used by the deterministic combine.
+/* Bytes of workspace for layers with k <= max_k and d_out <= max_d_out: a reserved 16 KB
+ * head, then the fp32 base output o_b (d_out) handed from the GEMV CTAs to the
+ * deterministic combine.  Every o_b entry is self-validating: it holds the pattern
+ * 0xFFFFFFFF (a NaN no arithmetic produces) until the GEMV stores it, and the combine
+ * restores the pattern after reading it, so no fence or arrival counter is needed.
  * (The paper's k x (4+2) B sc_indices / x[sc_indices] buffer lives in the shared
- * memory of each DEC CTA; max_k no longer changes the size, it is kept for ABI stability.) */
+ * memory of each DEC CTA; max_k does not change the size, it is kept for ABI stability.)
+ * A workspace serves one stream at a time; layers on that stream may share it. */
 size_t decdec_workspace_bytes(int32_t max_k, int32_t max_d_out);
 
-/* Zero a workspace (stream-ordered).  Required once before first use. */
+/* Initialise a workspace (stream-ordered): head zeroed, o_b set to the empty pattern.
+ * Required once before first use. */
 decdec_status decdec_workspace_init(void* ws, size_t ws_bytes, decdec_stream_t stream);
 
 /*

@@ -8,7 +8,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdecdec.so")
+# DECDEC_LIB: load another build of the same ABI (A/B timing of kernel variants on one box)
+LIB_PATH = os.environ.get("DECDEC_LIB") or os.path.join(_PKG, "libdecdec.so")
 
 DECDEC_OK = 0
 STATUS = {0: "DECDEC_OK", -1: "DECDEC_EINVAL", -2: "DECDEC_EALIGN", -3: "DECDEC_ENOTMAPPED",

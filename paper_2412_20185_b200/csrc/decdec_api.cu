@@ -36,7 +36,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 struct Plan {
   int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, n_dec;  // grid = GEMV CTAs (+ n_dec DEC CTAs)
-  int n_seg, rpi, gws;  // DEC: output segments, selected rows per gather item, items per segment
+  int n_seg, rpi, gws, nparts, one_seg;  // DEC: output segments, rows per gather item, items and partials per segment
   uint32_t stage_bytes, off_s, off_z, off_sel, off_x, off_part, off_rsc, off_stage;
   size_t smem;
 };
@@ -66,36 +66,44 @@ int dec_ctas(int warps_per_cta) {
 // smem: SelectSmem + staged x | idx, xs | partials [ns][gws][256] f32 | residual scales [ns][256].
 bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, Plan* p) {
   p->n_seg = (d_out + kSegCols - 1) / kSegCols;
+  static int env_rpi = -1;
+  if (env_rpi < 0) {
+    const char* e = getenv("DECDEC_GATHER_ROWS");
+    env_rpi = e ? atoi(e) : 0;
+  }
+  size_t sel_bytes = select_block_smem_bytes(sel_len);
+  if (sel_bytes < select_split_smem_bytes(sel_len)) sel_bytes = select_split_smem_bytes(sel_len);
+  const uint32_t off_sel = (uint32_t)align_up(sel_bytes, 16);
+  const uint32_t off_part = (uint32_t)align_up((size_t)off_sel + (size_t)k_sel * 6, 16);
+  const size_t row_b = max_rpi == kGatherRows16 ? 16 : 4;  // bytes per lane per staged row
   for (int nd = dec_ctas(warps); nd <= 64; nd *= 2) {
     const int ns = (p->n_seg + nd - 1) / nd;
     const int gws_target = (warps + ns - 1) / ns;
-    int rpi = (k_sel + gws_target - 1) / gws_target;
-    if (rpi > max_rpi) rpi = max_rpi;
-    if (rpi < 1) rpi = 1;
-    static int env_rpi = -1;
-    if (env_rpi < 0) {
-      const char* e = getenv("DECDEC_GATHER_ROWS");
-      env_rpi = e ? atoi(e) : 0;
+    // staging rows per buffer: as many as fit (<= max_rpi); fewer rows -> more, smaller items
+    for (int cap = max_rpi; cap >= 2; cap /= 2) {
+      int rpi = (k_sel + gws_target - 1) / gws_target;
+      if (rpi > cap) rpi = cap;
+      if (env_rpi > 0 && env_rpi < rpi) rpi = env_rpi;
+      if (rpi < 1) rpi = 1;
+      const int gws = (k_sel + rpi - 1) / rpi;
+      const int one_seg = ns == 1;
+      const int nparts = one_seg ? (gws < warps ? gws : warps) : gws;
+      const uint32_t off_rsc = off_part + (uint32_t)ns * nparts * kSegCols * 4;
+      const uint32_t off_stage = (uint32_t)align_up((size_t)off_rsc + (size_t)ns * kSegCols * 2, 16);
+      const size_t dec = off_stage + (size_t)warps * 2 * rpi * 32 * row_b;
+      if (dec > kSmemBudget + 16 * 1024) continue;
+      p->n_dec = nd;
+      p->rpi = rpi;
+      p->gws = gws;
+      p->nparts = nparts;
+      p->one_seg = one_seg;
+      p->off_sel = off_sel;
+      p->off_part = off_part;
+      p->off_rsc = off_rsc;
+      p->off_stage = off_stage;
+      if (dec > p->smem) p->smem = dec;
+      return true;
     }
-    if (env_rpi > 0 && env_rpi < rpi) rpi = env_rpi;
-    const int gws = (k_sel + rpi - 1) / rpi;
-    size_t sel_bytes = select_block_smem_bytes(sel_len);
-    if (sel_bytes < select_split_smem_bytes(sel_len)) sel_bytes = select_split_smem_bytes(sel_len);
-    const uint32_t off_sel = (uint32_t)align_up(sel_bytes, 16);
-    const uint32_t off_part = (uint32_t)align_up((size_t)off_sel + (size_t)k_sel * 6, 16);
-    const uint32_t off_rsc = off_part + (uint32_t)ns * gws * kSegCols * 4;
-    const uint32_t off_stage = (uint32_t)align_up((size_t)off_rsc + (size_t)ns * kSegCols * 2, 16);
-    const size_t dec = off_stage + (size_t)warps * 2 * 32 * 128;  // kGatherRows4 x u32 = kGatherRows16 x 16 B
-    if (dec > kSmemBudget + 16 * 1024) continue;
-    p->n_dec = nd;
-    p->rpi = rpi;
-    p->gws = gws;
-    p->off_sel = off_sel;
-    p->off_part = off_part;
-    p->off_rsc = off_rsc;
-    p->off_stage = off_stage;
-    if (dec > p->smem) p->smem = dec;
-    return true;
   }
   return false;
 }
@@ -179,7 +187,7 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
 struct WsLayout {
   size_t cnt, ob, total;
 };
-// workspace: per-segment o_b row counters, then o_b (fp32, d_out)
+// workspace: reserved head (16 KB), then o_b (fp32, d_out; self-validating, see ptx.cuh kObEmpty)
 WsLayout ws_layout(int k, int d_out) {
   (void)k;
   WsLayout w{};
@@ -337,8 +345,12 @@ size_t decdec_workspace_bytes(int32_t max_k, int32_t max_d_out) {
 }
 
 decdec_status decdec_workspace_init(void* ws, size_t ws_bytes, decdec_stream_t stream) {
-  if (!ws || ws_bytes < (size_t)kCntSlots * 4) return DECDEC_EINVAL;
-  return cuda_status(cudaMemsetAsync(ws, 0, ws_bytes, (cudaStream_t)stream));
+  const size_t head = ws_layout(0, 0).ob;
+  if (!ws || ws_bytes < head) return DECDEC_EINVAL;
+  cudaError_t e = cudaMemsetAsync(ws, 0, head, (cudaStream_t)stream);
+  if (e == cudaSuccess && ws_bytes > head)  // o_b entries = kObEmpty (0xFFFFFFFF)
+    e = cudaMemsetAsync(static_cast<uint8_t*>(ws) + head, 0xFF, ws_bytes - head, (cudaStream_t)stream);
+  return cuda_status(e);
 }
 
 int32_t decdec_num_selected(int32_t d_in, int32_t k, int32_t chunk) { return n_selected(d_in, k, chunk); }
@@ -415,14 +427,14 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
     p.r_scales = L->r_scales;
     p.r_row_bytes = L->d_out * L->r_bits / 8;
     p.ob = reinterpret_cast<float*>(base + wl.ob);
-    p.cnt = reinterpret_cast<uint32_t*>(base + wl.cnt);
     p.k_req = k;
     p.chunk = chunk;
     p.sel_out = sel;
     p.n_seg = P.pl.n_seg;
-    if (p.n_seg > kCntSlots - kCtrlSlots) return DECDEC_EUNSUPPORTED;
     p.rpi = P.pl.rpi;
     p.gws = P.pl.gws;
+    p.nparts = P.pl.nparts;
+    p.one_seg = P.pl.one_seg;
   }
   *out = P;
   return DECDEC_OK;

@@ -72,9 +72,10 @@ struct LinearParams {
   const uint8_t* r_rows;
   const uint16_t* r_scales;
   int r_row_bytes;
-  float* ob;      // workspace: fp32 o_b = W_hat x (GEMV CTAs -> DEC combine)
-  uint32_t* cnt;  // workspace: per-segment count of o_b rows written (reset by the combine)
-  int n_seg, gws;  // gws = gather items (partials) per segment
+  float* ob;      // workspace: fp32 o_b = W_hat x (GEMV CTAs -> DEC combine); kObEmpty = not yet written
+  int n_seg, gws;  // gws = gather items (row chunks) per segment
+  int nparts;      // partials per segment: min(gws, warps) when one_seg, else gws
+  int one_seg;     // n_seg <= n_dec: a DEC CTA owns at most one segment
   int rpi;               // selected rows per gather item (<= kGatherRows4 / kGatherRows16)
   // smem layout of a DEC CTA: SelectSmem, the staged x segment, idx int32[k_sel], xs u16[k_sel],
   // partials f32[ns][gws][kSegCols], residual scales u16[ns][kSegCols]
@@ -88,12 +89,6 @@ struct LinearParams {
   int prefetch;  // weight tiles requested per CTA before griddepcontrol.wait
   int* sel_out;
 };
-
-// GEMV side: publish `rows` o_b rows of segment `seg` (caller fenced its stores).
-__device__ __forceinline__ void gemv_publish(const LinearParams& p, int seg, uint32_t rows, int lane) {
-  __syncwarp();
-  if (lane == 0) atomicAdd(p.cnt + seg, rows);
-}
 
 // A DEC CTA (steps 1-4 of P:207).  DEC CTA c owns the output segments c, c + n_dec, ...:
 //   1. every DEC CTA computes the exact Top-k itself (same deterministic result, no hand-off);
@@ -111,7 +106,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   SelectSmemS* SS = reinterpret_cast<SelectSmemS*>(smem);  // split-order selector (aliases S)
   int* sidx = reinterpret_cast<int*>(smem + p.off_sel);
   uint16_t* sxs = reinterpret_cast<uint16_t*>(sidx + p.k_sel);
-  float* spart = reinterpret_cast<float*>(smem + p.off_part);    // [ns][gws][kSegCols]
+  float* spart = reinterpret_cast<float*>(smem + p.off_part);    // [ns][nparts][kSegCols]
   uint16_t* srsc = reinterpret_cast<uint16_t*>(smem + p.off_rsc);  // [ns][kSegCols] residual scales
   unsigned long long* tr = p.trace ? p.trace + blockIdx.x * kTraceEvents : nullptr;
   const int seg_len = p.chunk ? min(p.chunk, p.d_in) : p.d_in;
@@ -135,17 +130,19 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   using Vec = typename std::conditional<RBITS == 4, uint32_t, uint4>::type;
   constexpr int kGR = RBITS == 4 ? kGatherRows4 : kGatherRows16;
   // per-warp staging: 2 buffers x kGR rows x 32 lanes x Vec (cp.async destinations)
-  Vec* stage = reinterpret_cast<Vec*>(smem + p.off_stage) + (size_t)warp * 2 * kGR * 32;
+  Vec* stage = reinterpret_cast<Vec*>(smem + p.off_stage) + (size_t)warp * 2 * p.rpi * 32;
   auto issue = [&](int it, int bsel) {  // all zero-copy reads of item `it` (async, into smem)
     const int i = it % ns, j = it / ns;
     const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
     const bool cv = col0 < p.d_out;
     const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
-    Vec* dst = stage + bsel * kGR * 32 + lane;
+    Vec* dst = stage + bsel * p.rpi * 32 + lane;
+    if (RBITS == 4 && j == 0 && cv)  // all scale factors are fetched every call
+      cp_async_16(srsc + i * kSegCols + lane * 8, p.r_scales + col0);
 #pragma unroll
     for (int r = 0; r < kGR; ++r) {
       const int e = e0 + r;
-      if (e < e1 && cv) {
+      if (r < p.rpi && e < e1 && cv) {
         const uint8_t* rowp = p.r_rows + (size_t)sidx[e] * p.r_row_bytes;
         if constexpr (RBITS == 4) cp_async_4(dst + r * 32, rowp + (col0 >> 1));
         else cp_async_16(dst + r * 32, rowp + col0 * 2);
@@ -153,18 +150,15 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     }
     cp_async_commit();
   };
-  auto consume = [&](int it, int bsel) {  // decode + FHFMA, partial into smem
+  auto consume = [&](int it, int bsel, float* acc) {  // decode + FHFMA into acc[8]
     const int i = it % ns, j = it / ns;
     const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
     const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
-    if (RBITS == 4 && j == 0 && col0 < p.d_out)  // all scale factors are fetched every call
-      *reinterpret_cast<uint4*>(srsc + i * kSegCols + lane * 8) = ld_zc_u4(p.r_scales + col0);
-    const Vec* src = stage + bsel * kGR * 32 + lane;
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const Vec* src = stage + bsel * p.rpi * 32 + lane;
 #pragma unroll
     for (int r = 0; r < kGR; ++r) {
       const int e = e0 + r;
-      if (e < e1) {
+      if (r < p.rpi && e < e1) {
         const uint16_t xv = sxs[e];
         const Vec w = src[r * 32];
         uint32_t cq[4];
@@ -180,9 +174,16 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
         }
       }
     }
-    float* pp = spart + ((size_t)i * p.gws + j) * kSegCols + lane * 8;
+  };
+  // Partials: with one local segment (ns == 1) a warp's items all belong to it, so the warp
+  // accumulates them in registers and leaves ONE partial (slot = warp); otherwise one partial
+  // per item (slot = row chunk j).  p.nparts = partials per segment (combined in slot order).
+  auto store_part = [&](int i, int slot, float* acc) {
+    float* pp = spart + ((size_t)i * p.nparts + slot) * kSegCols + lane * 8;
     *reinterpret_cast<float4*>(pp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     *reinterpret_cast<float4*>(pp + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.f;
   };
   int it = warp;
   // ---- step 1: exact Top-k (whole x, or per chunk), S and x[S] into smem.  In global mode the
@@ -243,6 +244,9 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     ready(it);
     issue(it, 0);
   }
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool one_seg = p.one_seg;  // plan-wide: every DEC CTA has <= 1 segment
+  const bool had_item = it < n_items;
   for (int b = 0; it < n_items; b ^= 1, it += nw) {
     if (it + nw < n_items) {
       ready(it + nw);
@@ -251,25 +255,29 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     } else {
       cp_async_wait<0>();
     }
-    consume(it, b);
+    consume(it, b, acc);
+    if (!one_seg) store_part(it % ns, it / ns, acc);
   }
+  if (one_seg && had_item) store_part(0, warp, acc);
   if (lane == 0 && (warp == 0 || warp == nw - 1)) DECDEC_TRACE(p, warp == 0 ? 7 : 1);  // gather done
   __syncthreads();  // all partials of the CTA's segments are in smem
   if (threadIdx.x == 0) DECDEC_TRACE(p, 12);
-  // ---- step 4: combine, one warp per local segment
+  // ---- step 4: combine, one warp per local segment.  o_b entries are self-validating (relaxed
+  // stores of the GEMV CTAs, kObEmpty until written): poll them, then restore kObEmpty.
   for (int i = warp; i < ns; i += nw) {
     const int seg = (int)blockIdx.x + i * p.n_dec;
     const int col0 = seg * kSegCols + lane * 8;
-    const uint32_t seg_cols = (uint32_t)min(kSegCols, p.d_out - seg * kSegCols);
-    if (lane == 0) {
-      while (ld_acquire_gpu(p.cnt + seg) != seg_cols) __nanosleep(32);  // acquire: the o_b rows
-    }
-    __syncwarp();  // orders the lanes' (L2) loads after lane 0's acquire
     if (col0 < p.d_out) {
-      const float4 o0 = ld_cg_f4(p.ob + col0), o1 = ld_cg_f4(p.ob + col0 + 4);
+      uint4 o0 = ld_relaxed_gpu_u4(p.ob + col0), o1 = ld_relaxed_gpu_u4(p.ob + col0 + 4);
+      while ((o0.x == kObEmpty) | (o0.y == kObEmpty) | (o0.z == kObEmpty) | (o0.w == kObEmpty) |
+             (o1.x == kObEmpty) | (o1.y == kObEmpty) | (o1.z == kObEmpty) | (o1.w == kObEmpty)) {
+        __nanosleep(32);
+        o0 = ld_relaxed_gpu_u4(p.ob + col0);
+        o1 = ld_relaxed_gpu_u4(p.ob + col0 + 4);
+      }
       float sum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int j = 0; j < p.gws; ++j) {  // fixed order: row chunks ascending
-        const float* pp = spart + ((size_t)i * p.gws + j) * kSegCols + lane * 8;
+      for (int j = 0; j < p.nparts; ++j) {  // fixed order: slots ascending
+        const float* pp = spart + ((size_t)i * p.nparts + j) * kSegCols + lane * 8;
         const float4 a = *reinterpret_cast<const float4*>(pp), b = *reinterpret_cast<const float4*>(pp + 4);
         sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
         sum[4] += b.x; sum[5] += b.y; sum[6] += b.z; sum[7] += b.w;
@@ -284,7 +292,8 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
           Sc[2 * e + 1] = __half2float(__ushort_as_half((unsigned short)(sw[e] >> 16)));
         }
       }
-      const float o[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+      const float o[8] = {__uint_as_float(o0.x), __uint_as_float(o0.y), __uint_as_float(o0.z), __uint_as_float(o0.w),
+                          __uint_as_float(o1.x), __uint_as_float(o1.y), __uint_as_float(o1.z), __uint_as_float(o1.w)};
       uint32_t out[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -293,8 +302,10 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
         out[e] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
       }
       *reinterpret_cast<uint4*>(p.y + col0) = make_uint4(out[0], out[1], out[2], out[3]);
+      const uint4 empty = make_uint4(kObEmpty, kObEmpty, kObEmpty, kObEmpty);
+      *reinterpret_cast<uint4*>(p.ob + col0) = empty;  // ready for the next call
+      *reinterpret_cast<uint4*>(p.ob + col0 + 4) = empty;
     }
-    if (lane == 0) p.cnt[seg] = 0;  // ready for the next call
   }
   if (threadIdx.x == 0) DECDEC_TRACE(p, 9);
 }
@@ -550,7 +561,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
             const int m = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
             const int row = tile * TR + slot + m * NSLOTS;
             if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
-            else p.ob[row] = v;
+            else st_relaxed_gpu_f32(p.ob + row, v);
           }
         } else if (G == 32 && RPS == 2) {
           const bool hi16 = lane & 16;
@@ -560,7 +571,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
           if ((lane & 15) == 0) {
             const int row = tile * TR + slot + (hi16 ? 1 : 0) * NSLOTS;
             if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
-            else p.ob[row] = v;
+            else st_relaxed_gpu_f32(p.ob + row, v);
           }
         } else {
 #pragma unroll
@@ -571,7 +582,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
             if (g == 0) {
               const int row = tile * TR + slot + m * NSLOTS;
               if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
-              else p.ob[row] = v;
+              else st_relaxed_gpu_f32(p.ob + row, v);
             }
           }
         }
@@ -594,7 +605,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
             for (int w = 0; w < p.NKW; ++w) v += rbuf[lane * p.NKW + w];
             const int row = tile * TR + slot + lane * NSLOTS;
             if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
-            else p.ob[row] = v;
+            else st_relaxed_gpu_f32(p.ob + row, v);
           }
           nrows = RPS;
         }
@@ -606,14 +617,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       }
     }
     if (ct == 0) DECDEC_TRACE(p, 4);
-    // Publish o_b rows once per warp (one fence for all tiles, then one arrival per tile):
-    // a fence per tile stalled the GEMV stream by ~1 µs each.
-    if (p.k_sel > 0 && nrows_tile > 0) {
-      __threadfence();
-      for (int tile = cta; tile < p.n_tiles; tile += n_cta)
-        gemv_publish(p, (tile * TR) / kSegCols, (uint32_t)nrows_tile, lane);
-    }
-    if (ct == 0) DECDEC_TRACE(p, 10);  // o_b published (this warp)
+    if (ct == 0) DECDEC_TRACE(p, 10);  // last o_b row stored (this warp)
     return;
   }
 }

@@ -138,6 +138,20 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 }
 
 // ---------------------------------------------------------------- tracing (debug timelines)
+// self-validating o_b entries (GEMV CTAs -> DEC combine, no fence, no counter): each fp32 is
+// stored once with a relaxed gpu-scope store and polled with relaxed gpu-scope loads until it is
+// no longer the kObEmpty pattern (a NaN no arithmetic produces; the reader restores it).
+constexpr uint32_t kObEmpty = 0xFFFFFFFFu;
+__device__ __forceinline__ void st_relaxed_gpu_f32(float* p, float v) {
+  asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ uint4 ld_relaxed_gpu_u4(const void* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -414,7 +414,7 @@ __device__ __forceinline__ void select_block_regs(const uint16_t* __restrict__ x
 // Returns D.  The caller's warps may use positions < D immediately; positions >= D after
 // select_wait_rest().  If sel_out is non-null the finisher also writes the whole selection
 // in ascending index order (merge of the two sorted runs; the decdec_linear `sel` contract).
-constexpr int kCandList = 64;  // threshold-bin candidates kept as a sortable list (else bitmap scan)
+constexpr int kCandList = 256;  // threshold-bin candidates kept as a sortable list (else bitmap scan)
 struct SelectSmemS {
   SelectSmemR r;
   uint32_t bitmap[1024];  // threshold-bin candidates, bit i = key i (n <= 32768)
@@ -436,6 +436,68 @@ __device__ __forceinline__ void select_split_zero(SelectSmemS* S, int n) {
 __device__ __forceinline__ void select_wait_rest(const SelectSmemS* S) {
   while (*reinterpret_cast<const volatile uint32_t*>(&S->rest_ready) == 0u) __nanosleep(100);  // keep the LSU free
   __threadfence_block();
+}
+
+// Finisher (one warp): sort the threshold-bin candidates (index << 15 | key) by index with a
+// warp bitonic network over 32*E slots (E per lane, slot = lane + 32 h), then write the taken
+// ones (key > T, or key == T among the first `need` ties) at positions nD.. in index order.
+template <int E>
+__device__ __forceinline__ void select_finish_list(const SelectSmemS* SS, const uint16_t* __restrict__ x, uint32_t ncand,
+                                                   uint32_t T, uint32_t need, uint32_t nD, int* __restrict__ idx_out,
+                                                   uint16_t* __restrict__ xs_out) {
+  const int lane = threadIdx.x & 31;
+  constexpr int N = 32 * E;
+  uint32_t e[E];
+#pragma unroll
+  for (int h = 0; h < E; ++h) e[h] = (uint32_t)(lane + 32 * h) < ncand ? SS->cand[lane + 32 * h] : 0xffffffffu;
+#pragma unroll
+  for (int k2 = 2; k2 <= N; k2 <<= 1) {
+#pragma unroll
+    for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+      if (j2 >= 32) {  // partner in the same lane: slot h ^ (j2 / 32)
+        const int jh = j2 >> 5;
+#pragma unroll
+        for (int h = 0; h < E; ++h) {
+          if (h & jh) continue;
+          const int pos = lane + 32 * h;
+          const bool up = (pos & k2) == 0;
+          const uint32_t lo = min(e[h], e[h | jh]), hi = max(e[h], e[h | jh]);
+          e[h] = up ? lo : hi;
+          e[h | jh] = up ? hi : lo;
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < E; ++h) {
+          const int pos = lane + 32 * h;
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, e[h], j2);
+          const bool up = (pos & k2) == 0;
+          const bool lower = (pos & j2) == 0;
+          e[h] = (lower == up) ? min(e[h], o) : max(e[h], o);
+        }
+      }
+    }
+  }
+  // slots are now in index order along (h, lane)
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t taken_before = 0, eq_before = 0;
+#pragma unroll
+  for (int h = 0; h < E; ++h) {
+    const uint32_t v = e[h];
+    const bool valid = v != 0xffffffffu;
+    const uint32_t key = v & 0x7fffu;
+    const bool gt = valid && key > T, eq = valid && key == T;
+    const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+    const uint32_t my_eq = eq_before + __popc(beq & lt);
+    const bool take = gt || (eq && my_eq < need);
+    const uint32_t bt = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      const uint32_t pos = nD + taken_before + __popc(bt & lt);
+      idx_out[pos] = (int)(v >> 15);
+      xs_out[pos] = x[v >> 15];
+    }
+    taken_before += __popc(bt);
+    eq_before += __popc(beq);
+  }
 }
 
 template <int MAXC>
@@ -482,30 +544,49 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
   }
   SEL_TRACE(17);
   // ---- D counts; fine histogram + candidate bitmap/list of bin bA.  Per chunk the per-key
-  // work is branch-free (masks); the rare keys in bin bA take one branch per chunk.
-  uint32_t n_d = 0, dmask[MAXC];
+  // work is branch-free (masks); the rare keys in bin bA take one branch per chunk.  List slots
+  // are allocated once per warp (scan of the lanes' candidate counts, one atomic by lane 31):
+  // per-chunk atomics on the shared counter serialised into ~1 us on d-sized inputs.
+  uint32_t n_d = 0, n_c = 0, dmask[MAXC], cmask[MAXC];
 #pragma unroll
   for (int m = 0; m < MAXC; ++m) {
     dmask[m] = 0;
+    cmask[m] = 0;
     if (m < nv) {
-      uint32_t bits = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint32_t b = (chunk_elem(v[m], j) & 0x7fffu) >> 7;
         dmask[m] |= (uint32_t)(b > bA) << j;
-        bits |= (uint32_t)(b == bA) << j;
+        cmask[m] |= (uint32_t)(b == bA) << j;
       }
       n_d += __popc(dmask[m]);
-      if (bits) {
-        atomicOr(&SS->bitmap[(c0 + m) >> 2], bits << (8 * ((c0 + m) & 3)));
-        const uint32_t slot = atomicAdd(&SS->ncand, (uint32_t)__popc(bits));
-        uint32_t o = slot;
-        for (uint32_t bb = bits; bb; bb &= bb - 1, ++o) {
-          const int jj = __ffs(bb) - 1;
-          const uint32_t key = chunk_elem(v[m], jj) & 0x7fffu;
-          const uint32_t fb = key & 127u;
-          atomicAdd(&S->histB[fb + (fb >> 2)], 1u);
-          if (o < (uint32_t)kCandList) SS->cand[o] = ((uint32_t)(8 * (c0 + m) + jj) << 15) | key;
+      n_c += __popc(cmask[m]);
+    }
+  }
+  {
+    uint32_t inc_c = n_c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc_c, o);
+      if (lane >= o) inc_c += u;
+    }
+    uint32_t base = 0;
+    if (lane == 31 && inc_c) base = atomicAdd(&SS->ncand, inc_c);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    uint32_t o = base + inc_c - n_c;  // this thread's first list slot
+    if (n_c) {
+#pragma unroll
+      for (int m = 0; m < MAXC; ++m) {
+        const uint32_t bits = cmask[m];
+        if (bits) {
+          atomicOr(&SS->bitmap[(c0 + m) >> 2], bits << (8 * ((c0 + m) & 3)));
+          for (uint32_t bb = bits; bb; bb &= bb - 1, ++o) {
+            const int jj = __ffs(bb) - 1;
+            const uint32_t key = chunk_elem(v[m], jj) & 0x7fffu;
+            const uint32_t fb = key & 127u;
+            atomicAdd(&S->histB[fb + (fb >> 2)], 1u);
+            if (o < (uint32_t)kCandList) SS->cand[o] = ((uint32_t)(8 * (c0 + m) + jj) << 15) | key;
+          }
         }
       }
     }
@@ -556,53 +637,10 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
     }
     if (tr && lane == 0) tr[11] = clock64();
     const uint32_t ncand = SS->ncand;
-    if (ncand <= (uint32_t)kCandList) {
-      // sort the candidates by index (bitonic over 64 = 2 per lane, keys ride in the low bits)
-      uint32_t e0 = lane < (int)ncand ? SS->cand[lane] : 0xffffffffu;
-      uint32_t e1 = lane + 32 < (int)ncand ? SS->cand[lane + 32] : 0xffffffffu;
-#pragma unroll
-      for (int k2 = 2; k2 <= 64; k2 <<= 1) {
-#pragma unroll
-        for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-          if (j2 == 32) {  // partner in the other half, same lane
-            const bool up = ((lane & k2) == 0);  // k2 == 64: always ascending
-            const uint32_t lo = min(e0, e1), hi = max(e0, e1);
-            e0 = up ? lo : hi;
-            e1 = up ? hi : lo;
-          } else {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int pos = lane + 32 * h;
-              uint32_t& e = h ? e1 : e0;
-              const uint32_t o = __shfl_xor_sync(0xffffffffu, e, j2);
-              const bool up = ((pos & k2) == 0);
-              const bool lower = (pos & j2) == 0;
-              e = (lower == up) ? min(e, o) : max(e, o);
-            }
-          }
-        }
-      }
-      // positions in index order: taken = key > T, or key == T among the first `need` ties
-      const uint32_t lt = (1u << lane) - 1u;
-      uint32_t taken_before = 0, eq_before = 0;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t e = h ? e1 : e0;
-        const bool valid = e != 0xffffffffu;
-        const uint32_t key = e & 0x7fffu;
-        const bool gt = valid && key > T, eq = valid && key == T;
-        const uint32_t beq = __ballot_sync(0xffffffffu, eq);
-        const uint32_t my_eq = eq_before + __popc(beq & lt);
-        const bool take = gt || (eq && my_eq < need);
-        const uint32_t bt = __ballot_sync(0xffffffffu, take);
-        if (take) {
-          const uint32_t pos = nD + taken_before + __popc(bt & lt);
-          idx_out[pos] = (int)(e >> 15);
-          xs_out[pos] = x[e >> 15];
-        }
-        taken_before += __popc(bt);
-        eq_before += __popc(beq);
-      }
+    if (ncand <= 64u) {
+      select_finish_list<2>(SS, x, ncand, T, need, nD, idx_out, xs_out);
+    } else if (ncand <= (uint32_t)kCandList) {
+      select_finish_list<kCandList / 32>(SS, x, ncand, T, need, nD, idx_out, xs_out);
     } else {
     const int nwords = (n + 31) >> 5;
     const int W = (nwords + 31) >> 5;  // lane l owns bitmap words [l*W, l*W + W): index order

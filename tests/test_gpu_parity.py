@@ -151,6 +151,50 @@ def test_llama_shapes_sampled(bits, name):
             assert ok.all(), (name, bits, kc, err[~ok][:5], bound[~ok][:5])
 
 
+# ------------------------------------------------------------------ Phi-3 / Llama-3-70B shards (configs 4/5)
+@pytest.mark.parametrize("model,name,P", [("phi3_medium", "qkv", 1), ("phi3_medium", "d", 1), ("phi3_medium", "o", 8),
+                                          ("phi3_medium", "gu", 8), ("llama3_70b", "qkv", 8), ("llama3_70b", "d", 8),
+                                          ("llama3_70b", "gu", 8)])
+def test_tp_shard_shapes_sampled(model, name, P):
+    """A rank's output-feature shard (d_out / P columns) at the BASELINE configs
+    4/5 shapes: selection bit-exact (identical on every rank), sampled outputs within L9."""
+    d_in, d_out = SHAPES[model][name]
+    d_r = d_out // P
+    L = gen_perf_layer(d_in, d_r, 3, seed=layer_seed(model, name, P))
+    lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"])
+    ws = dd.Workspace(oracle.k_from_kchunk(82, d_in), d_r)
+    rng = np.random.default_rng(1)
+    cols = np.unique(np.concatenate([rng.choice(d_r, min(d_r, 256), replace=False), [0, d_r - 1]]))
+    x = gen_activations(d_in, 1, seed=layer_seed(model, name, "x"), kind="d" if name == "d" else "qkv")[0]
+    xd = to_dev(x)
+    for kc in (0, 21, 82):
+        k = oracle.k_from_kchunk(kc, d_in)
+        sel = torch.empty(max(k, 1), dtype=torch.int32, device=DEV)
+        y = lin(xd, k, sel=sel, workspace=ws).cpu().numpy()
+        ref = oracle.decdec_linear_ref_cols(L["q"], L["s"], L["z"], x, k, cols, rc=L["rc"], rS=L["rS"])
+        if k:
+            assert np.array_equal(sel.cpu().numpy(), ref["idx"])
+        ok, err, bound = tolerance_ok(y[cols], ref["y64"], ref["A"])
+        assert ok.all(), (model, name, P, kc, err[~ok][:5], bound[~ok][:5])
+
+
+@pytest.mark.parametrize("kind", ["all_equal", "zeros", "ties", "sparse"])
+def test_fused_selection_ties_and_degenerate(kind):
+    """The fused layer kernel's own (split-order) selector on tie-heavy / degenerate x: the
+    threshold bin then holds thousands of candidates (bitmap path) or all keys are equal."""
+    for d_in, d_out in ((4096, 1024), (14336, 512)):
+        L = gen_perf_layer(d_in, d_out, 3, seed=layer_seed("fused_ties", d_in))
+        lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"])
+        ws = dd.Workspace(d_in // 2, d_out)
+        x = gen_special_activations(d_in, kind, seed=d_in + 1)
+        for k in (1, 3, 100, d_in // 5):
+            sel = torch.empty(k, dtype=torch.int32, device=DEV)
+            y = lin(to_dev(x), k, sel=sel, workspace=ws)
+            ref = decdec_linear_ref(L["q"], L["s"], L["z"], x, k, rc=L["rc"], rS=L["rS"])
+            assert np.array_equal(sel.cpu().numpy(), ref["idx"]), (kind, d_in, k)
+            check_close(y, ref, f"fused ties {kind} d_in={d_in} k={k}")
+
+
 def test_chunk_mode_linear():
     d_in, d_out = 5120, 640   # Phi-3 o shard at P=8; 5 chunks
     L = gen_perf_layer(d_in, d_out, 3, seed=11)
