@@ -153,7 +153,7 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
         static int env_kb = -1;
         if (env_kb < 0) {
           const char* e = getenv("DECDEC_INFLIGHT_KB");
-          env_kb = e ? atoi(e) : 64;
+          env_kb = e ? atoi(e) : 128;
         }
         int cap = (int)(((size_t)env_kb * 1024) / p.stage_bytes);
         if (cap < 2) cap = 2;
@@ -329,7 +329,7 @@ LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, 
   static int env_prefetch = -1;
   if (env_prefetch < 0) {
     const char* e = getenv("DECDEC_PREFETCH");
-    env_prefetch = e ? atoi(e) : 1;
+    env_prefetch = e ? atoi(e) : 8;
   }
   p.prefetch = env_prefetch;
   return p;

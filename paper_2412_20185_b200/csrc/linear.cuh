@@ -151,8 +151,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     cp_async_commit();
   };
   auto consume = [&](int it, int bsel, float* acc) {  // decode + FHFMA into acc[8]
-    const int i = it % ns, j = it / ns;
-    const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
+    const int j = it / ns;
     const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
     const Vec* src = stage + bsel * p.rpi * 32 + lane;
 #pragma unroll
