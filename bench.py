@@ -325,33 +325,19 @@ def main():
     torch.cuda.synchronize()
     t_build = time.time() - t_build
     n_layers = len(M.meta)
+    comm = dd.Comm() if world > 1 else None  # library-owned NCCL communicator (TP all-gather)
 
     # ---- full decode-step graphs per k_chunk -------------------------------------------------
     def step_launchers(kc):
         if world == 1:
             stacks = [dd.Stack(M.layers, M.ks(kc), M.xs(s), M.ys(), ws) for s in range(args.nx)]
             return stacks, [st.launch for st in stacks], stacks[0].kernels
-        # TP: per-layer decdec_linear on the shard + NCCL all-gather, captured by torch.cuda.graph
+        # TP: decdec_stack_create_tp -- every layer on this rank's shard + the library's in-place
+        # NCCL all-gather of y, captured as one native CUDA graph
         full = [torch.empty(m[3] * world, dtype=torch.float16, device=dev) for m in M.meta]
-        graphs = []
-        for s in range(args.nx):
-            xs, ys = M.xs(s), M.ys()
-            g = torch.cuda.CUDAGraph()
-            side = torch.cuda.Stream()
-            side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side):
-                for i, lin in enumerate(M.layers):   # warm NCCL outside capture
-                    lin(xs[i], M.ks(kc, [i])[0], y=ys[i], workspace=ws)
-                    dist.all_gather_into_tensor(full[i], ys[i])
-            torch.cuda.current_stream().wait_stream(side)
-            torch.cuda.synchronize()
-            with torch.cuda.graph(g, capture_error_mode="relaxed"):
-                for i, lin in enumerate(M.layers):
-                    lin(xs[i], M.ks(kc, [i])[0], y=ys[i], workspace=ws)
-                    dist.all_gather_into_tensor(full[i], ys[i])
-            graphs.append(g)
-        kern = sum(2 if k else 1 for k in M.ks(kc))
-        return graphs, [g.replay for g in graphs], kern
+        stacks = [dd.TPStack(M.layers, M.ks(kc), M.xs(s), full, ws, comm) for s in range(args.nx)]
+        kern = stacks[0].kernels  # our kernels (+ one NCCL all-gather per layer, not counted)
+        return stacks, [st.launch for st in stacks], kern
 
     results = {}
     headline = None

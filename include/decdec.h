@@ -144,6 +144,45 @@ decdec_status decdec_stack_launch(decdec_stack* s, decdec_stream_t stream);
 int32_t decdec_stack_kernels(const decdec_stack* s); /* kernels per launch, -1 if NULL */
 void decdec_stack_destroy(decdec_stack* s);
 
+/* ------------------------------------------------------------------ tensor parallelism */
+/* Output-feature sharding (BASELINE.json north_star "the layer shards by
+ * output features ... output assembled with an NCCL all-gather over NVLink").  Rank r holds
+ * columns [r*d_out_r, (r+1)*d_out_r) of W_hat (its device memory) and of R_hat + scales (its
+ * own pinned host slice behind its own PCIe link); x is replicated, so every rank selects the
+ * identical S (exact, deterministic selector; ledger L11) and no index exchange is needed.
+ * The communicator is library-owned; NCCL is loaded at run time (dlopen of libnccl.so.2,
+ * reusing one already loaded in the process).  Errors: DECDEC_ENCCL if NCCL cannot be loaded
+ * or a NCCL call fails. */
+typedef struct decdec_comm decdec_comm;
+
+/* NCCL version code of the loaded library (e.g. 22809), -1 if NCCL cannot be loaded. */
+int32_t decdec_nccl_version(void);
+
+/* Fill id_out (128 bytes, host) with a new NCCL unique id.  Call on one rank and broadcast
+ * the bytes to the others out of band (e.g. the torch.distributed process group). */
+decdec_status decdec_nccl_unique_id(void* id_out);
+
+/* Collective over all nranks: create this rank's communicator on the current device. */
+decdec_status decdec_comm_init(const void* id, int32_t rank, int32_t nranks, decdec_comm** out);
+void decdec_comm_destroy(decdec_comm* c);
+int32_t decdec_comm_rank(const decdec_comm* c);   /* -1 if NULL */
+int32_t decdec_comm_nranks(const decdec_comm* c); /* -1 if NULL */
+
+/* decdec_linear on this rank's shard L (L->d_out = d_out_r), writing its outputs straight
+ * into y_full + rank*d_out_r, followed on the same stream by an in-place all-gather that
+ * leaves the full y (device fp16 [nranks*d_out_r], 16-B aligned) on every rank.  Every rank
+ * must call it with the same x, k, chunk and d_out_r.  sel/ws as decdec_linear. */
+decdec_status decdec_linear_tp(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk,
+                               uint16_t* y_full, int32_t* sel, void* ws, size_t ws_bytes, decdec_comm* comm,
+                               decdec_stream_t stream);
+
+/* A TP decode step captured as one CUDA graph: for each layer i, decdec_linear on the shard
+ * into y_full[i] + rank*d_out_r(i), then the in-place all-gather of y_full[i]
+ * ([nranks*layers[i].d_out]).  Launch/destroy with decdec_stack_launch/_destroy. */
+decdec_status decdec_stack_create_tp(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
+                                     const uint16_t* const* x, uint16_t* const* y_full, void* ws, size_t ws_bytes,
+                                     decdec_comm* comm, decdec_stream_t stream, decdec_stack** out);
+
 /* ------------------------------------------------------------------ offline, host-only */
 /* Pack base codes q (u8 [d_in][d_out], logical W layout, values < 2^bits) into W3K/W4K
  * (uint32 [d_out][d_in*bits/32]).  out_bytes must be >= d_out*d_in*bits/8. */

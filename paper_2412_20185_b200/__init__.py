@@ -10,6 +10,10 @@ from ._lib import (  # noqa: F401
     EXPORTED,
     LIB_PATH,
     DecdecError,
+    decdec_comm_destroy,
+    decdec_comm_init,
+    decdec_comm_nranks,
+    decdec_comm_rank,
     decdec_debug_trace,
     decdec_debug_unpack_weights,
     decdec_gemv,
@@ -18,12 +22,16 @@ from ._lib import (  # noqa: F401
     decdec_launches_per_call,
     decdec_layer,
     decdec_linear,
+    decdec_linear_tp,
+    decdec_nccl_unique_id,
+    decdec_nccl_version,
     decdec_num_selected,
     decdec_pack_residual,
     decdec_pack_weights,
     decdec_plan_string,
     decdec_select,
     decdec_stack_create,
+    decdec_stack_create_tp,
     decdec_stack_destroy,
     decdec_stack_kernels,
     decdec_stack_launch,
@@ -32,4 +40,5 @@ from ._lib import (  # noqa: F401
     decdec_workspace_bytes,
     decdec_workspace_init,
 )
+from .tp import Comm, TPLinear, TPStack, shard_codes, shard_columns  # noqa: F401
 from .layer import HostBuffer, QuantLinear, Stack, Workspace, pack_residual_into, pack_weights, select  # noqa: F401

@@ -61,6 +61,14 @@ def _load():
         "decdec_stack_destroy": (None, [VP]),
         "decdec_status_string": (ctypes.c_char_p, [I32]),
         "decdec_version": (ctypes.c_char_p, []),
+        "decdec_nccl_version": (I32, []),
+        "decdec_nccl_unique_id": (I32, [VP]),
+        "decdec_comm_init": (I32, [VP, I32, I32, P(VP)]),
+        "decdec_comm_destroy": (None, [VP]),
+        "decdec_comm_rank": (I32, [VP]),
+        "decdec_comm_nranks": (I32, [VP]),
+        "decdec_linear_tp": (I32, [Lp, VP, I32, I32, VP, VP, VP, SZ, VP, VP]),
+        "decdec_stack_create_tp": (I32, [Lp, I32, P(I32), I32, P(VP), P(VP), VP, SZ, VP, VP, P(VP)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -76,6 +84,8 @@ EXPORTED = [
     "decdec_host_free", "decdec_debug_unpack_weights", "decdec_plan_string", "decdec_launches_per_call",
     "decdec_status_string", "decdec_version", "decdec_stack_create", "decdec_stack_launch",
     "decdec_stack_kernels", "decdec_stack_destroy", "decdec_debug_trace",
+    "decdec_nccl_version", "decdec_nccl_unique_id", "decdec_comm_init", "decdec_comm_destroy",
+    "decdec_comm_rank", "decdec_comm_nranks", "decdec_linear_tp", "decdec_stack_create_tp",
 ]
 
 
@@ -180,3 +190,52 @@ def decdec_stack_destroy(s):
 
 def decdec_debug_trace(buf, nbytes):
     _check(_lib.decdec_debug_trace(_vp(buf), nbytes), "decdec_debug_trace")
+
+
+# ------------------------------------------------------------------ tensor parallelism
+def decdec_nccl_version() -> int:
+    return int(_lib.decdec_nccl_version())
+
+
+def decdec_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.decdec_nccl_unique_id(buf), "decdec_nccl_unique_id")
+    return buf.raw
+
+
+def decdec_comm_init(uid: bytes, rank: int, nranks: int) -> int:
+    if len(uid) != 128:
+        raise ValueError("NCCL unique id must be 128 bytes")
+    buf = ctypes.create_string_buffer(uid, 128)
+    out = ctypes.c_void_p()
+    _check(_lib.decdec_comm_init(buf, rank, nranks, ctypes.byref(out)), "decdec_comm_init")
+    return int(out.value)
+
+
+def decdec_comm_destroy(c):
+    _lib.decdec_comm_destroy(_vp(c))
+
+
+def decdec_comm_rank(c) -> int:
+    return int(_lib.decdec_comm_rank(_vp(c)))
+
+
+def decdec_comm_nranks(c) -> int:
+    return int(_lib.decdec_comm_nranks(_vp(c)))
+
+
+def decdec_linear_tp(L: decdec_layer, x, k: int, chunk: int, y_full, sel, ws, ws_bytes: int, comm, stream=0):
+    _check(_lib.decdec_linear_tp(ctypes.byref(L), _vp(x), k, chunk, _vp(y_full), _vp(sel), _vp(ws), ws_bytes,
+                                 _vp(comm), _vp(stream)), "decdec_linear_tp")
+
+
+def decdec_stack_create_tp(layers, ks, chunk, xs, ys_full, ws, ws_bytes, comm, stream=0) -> int:
+    n = len(layers)
+    arr = (decdec_layer * n)(*layers)
+    karr = (ctypes.c_int32 * n)(*[int(k) for k in ks])
+    xarr = (ctypes.c_void_p * n)(*[int(p) for p in xs])
+    yarr = (ctypes.c_void_p * n)(*[int(p) for p in ys_full])
+    out = ctypes.c_void_p()
+    _check(_lib.decdec_stack_create_tp(arr, n, karr, chunk, xarr, yarr, _vp(ws), ws_bytes, _vp(comm), _vp(stream),
+                                       ctypes.byref(out)), "decdec_stack_create_tp")
+    return int(out.value)

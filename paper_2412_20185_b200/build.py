@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
         "-cudart", "shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC, *os.environ.get("DECDEC_NVCC_EXTRA", "").split(),
         "-Xptxas", "-v" if verbose else "-O3",
-        "-o", LIB + ".tmp", *sources(),
+        "-o", LIB + ".tmp", *sources(), "-ldl",
     ]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -9,6 +9,7 @@
 #include "decdec.h"
 #include "linear.cuh"
 #include "select.cuh"
+#include "tp_internal.h"
 
 using namespace decdec;
 
@@ -464,16 +465,25 @@ decdec_status decdec_linear(const decdec_layer* L, const uint16_t* x, int32_t k,
   return enqueue_linear(P, (cudaStream_t)stream);
 }
 
-decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
-                                  const uint16_t* const* x, uint16_t* const* y, void* ws, size_t ws_bytes,
-                                  decdec_stream_t stream, decdec_stack** out) {
+}  // extern "C"
+
+namespace {
+
+// comm == nullptr: single-GPU stack; otherwise layer i writes y[i] + rank*d_out_r and is
+// followed by the in-place all-gather of y[i].
+decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
+                           const uint16_t* const* x, uint16_t* const* y, void* ws, size_t ws_bytes,
+                           decdec_comm* comm, decdec_stack** out) {
   if (!layers || n_layers <= 0 || !k || !x || !y || !out) return DECDEC_EINVAL;
   *out = nullptr;
+  const int rank = comm ? tp_rank(comm) : 0;
+  const bool gather = comm && decdec_comm_nranks(comm) > 1;
   Prepared* P = new Prepared[n_layers];
   decdec_status s = DECDEC_OK;
   int n_kernels = 0;
   for (int i = 0; i < n_layers && s == DECDEC_OK; ++i) {
-    s = prepare_linear(&layers[i], x[i], k[i], chunk, y[i], nullptr, ws, ws_bytes, &P[i]);
+    uint16_t* yi = y[i] ? y[i] + (size_t)rank * layers[i].d_out : nullptr;
+    s = prepare_linear(&layers[i], x[i], k[i], chunk, yi, nullptr, ws, ws_bytes, &P[i]);
     // debug timelines: one trace region per layer (decdec_debug_trace buffer must hold them)
     if (g_trace) P[i].p.trace = g_trace + 2 + (size_t)i * kTraceStride;
     n_kernels += 1;
@@ -482,7 +492,6 @@ decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, 
     delete[] P;
     return s;
   }
-  (void)stream;  // capture runs on a private stream (the legacy NULL stream cannot capture)
   cudaStream_t st = nullptr;
   cudaError_t e0 = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   if (e0 != cudaSuccess) {
@@ -491,7 +500,11 @@ decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, 
   }
   decdec_stack* g = new decdec_stack();
   cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
-  for (int i = 0; i < n_layers && e == cudaSuccess && s == DECDEC_OK; ++i) s = enqueue_linear(P[i], st, i > 0);
+  for (int i = 0; i < n_layers && e == cudaSuccess && s == DECDEC_OK; ++i) {
+    // PDL edges only between consecutive layer kernels (not across a collective)
+    s = enqueue_linear(P[i], st, i > 0 && !gather);
+    if (s == DECDEC_OK && gather) s = tp_allgather(comm, y[i], layers[i].d_out, st);
+  }
   cudaGraph_t graph = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(st, &graph);
   cudaStreamDestroy(st);
@@ -507,6 +520,25 @@ decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, 
   }
   *out = g;
   return DECDEC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+decdec_status decdec_stack_create(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
+                                  const uint16_t* const* x, uint16_t* const* y, void* ws, size_t ws_bytes,
+                                  decdec_stream_t stream, decdec_stack** out) {
+  (void)stream;  // capture runs on a private stream (the legacy NULL stream cannot capture)
+  return stack_create(layers, n_layers, k, chunk, x, y, ws, ws_bytes, nullptr, out);
+}
+
+decdec_status decdec_stack_create_tp(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
+                                     const uint16_t* const* x, uint16_t* const* y_full, void* ws, size_t ws_bytes,
+                                     decdec_comm* comm, decdec_stream_t stream, decdec_stack** out) {
+  (void)stream;
+  if (!comm) return DECDEC_EINVAL;
+  return stack_create(layers, n_layers, k, chunk, x, y_full, ws, ws_bytes, comm, out);
 }
 
 decdec_status decdec_stack_launch(decdec_stack* g, decdec_stream_t stream) {

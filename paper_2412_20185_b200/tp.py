@@ -4,7 +4,9 @@ Every rank holds a contiguous, 32-column-aligned slice of the output columns of 
 and of R_hat + its scales (its own pinned host slice, behind its own PCIe link).  x is
 replicated, so every rank computes the identical selection S locally (the selector is exact
 and deterministic) -- no index exchange.  The one real exchange step is assembling y: an
-NCCL all-gather of the fp16 shards over NVLink (PyTorch process group = plumbing).
+NCCL all-gather of the fp16 shards over NVLink, issued by the library (decdec_linear_tp /
+decdec_stack_create_tp) on a library-owned communicator; the PyTorch process group only carries
+the NCCL unique id (plumbing).
 """
 
 from __future__ import annotations
@@ -40,25 +42,94 @@ def shard_codes(layer: dict, rank: int, world: int) -> dict:
     return out
 
 
-class TPLinear:
-    """This rank's shard of a DecDEC layer + the all-gather that assembles y."""
+def broadcast_unique_id(group=None, make_id=None) -> bytes:
+    """Rank 0 creates the 128-byte NCCL unique id (decdec_nccl_unique_id) and broadcasts it over
+    the torch.distributed process group (plumbing only); every rank returns the same bytes."""
+    import torch.distributed as dist
 
-    def __init__(self, shard_linear, group=None):
+    if make_id is None:
+        from paper_2412_20185_b200 import _lib
+
+        make_id = _lib.decdec_nccl_unique_id
+    obj = [make_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return obj[0]
+
+
+class Comm:
+    """Library-owned NCCL communicator (decdec_comm_init) over the ranks of a torch PG."""
+
+    def __init__(self, group=None):
         import torch.distributed as dist
+        from paper_2412_20185_b200 import _lib
 
+        self._lib = _lib
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.handle = _lib.decdec_comm_init(broadcast_unique_id(group), self.rank, self.world)
+
+    def close(self):
+        if self.handle:
+            self._lib.decdec_comm_destroy(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class TPLinear:
+    """This rank's shard of a DecDEC layer; decdec_linear_tp runs the shard and the in-place
+    NCCL all-gather that assembles y on every rank (one C-ABI call)."""
+
+    def __init__(self, shard_linear, comm: Comm):
         self.lin = shard_linear
-        self.group = group
-        self.world = dist.get_world_size(group)
+        self.comm = comm
+        self.world = comm.world
         self.d_out_shard = shard_linear.d_out
 
-    def __call__(self, x, k: int, chunk: int = 0, y_full=None, y_shard=None, sel=None, workspace=None):
+    def __call__(self, x, k: int, chunk: int = 0, y_full=None, sel=None, workspace=None, stream=None):
         import torch
-        import torch.distributed as dist
+        from paper_2412_20185_b200 import _lib
+        from paper_2412_20185_b200.layer import Workspace, _stream_ptr
 
-        if y_shard is None:
-            y_shard = torch.empty(self.d_out_shard, dtype=torch.float16, device=x.device)
         if y_full is None:
             y_full = torch.empty(self.d_out_shard * self.world, dtype=torch.float16, device=x.device)
-        self.lin(x, k, chunk, y=y_shard, sel=sel, workspace=workspace)
-        dist.all_gather_into_tensor(y_full, y_shard, group=self.group)
+        if workspace is None:
+            workspace = Workspace(max(k, 1), self.d_out_shard)
+        _lib.decdec_linear_tp(self.lin.struct, x.data_ptr(), k, chunk, y_full.data_ptr(),
+                              sel.data_ptr() if sel is not None else 0, workspace.ptr, workspace.nbytes,
+                              self.comm.handle, _stream_ptr(stream))
         return y_full
+
+
+class TPStack:
+    """A TP decode step (every layer on its shard + all-gather) as one native CUDA graph
+    (decdec_stack_create_tp); launch/close like layer.Stack."""
+
+    def __init__(self, layers, ks, xs, ys_full, workspace, comm: Comm, chunk: int = 0):
+        from paper_2412_20185_b200 import _lib
+
+        self._lib = _lib
+        self._keep = (list(layers), list(xs), list(ys_full), workspace, comm)
+        self.handle = _lib.decdec_stack_create_tp([l.struct for l in layers], ks, chunk,
+                                                  [x.data_ptr() for x in xs], [y.data_ptr() for y in ys_full],
+                                                  workspace.ptr, workspace.nbytes, comm.handle, 0)
+        self.kernels = _lib.decdec_stack_kernels(self.handle)
+
+    def launch(self, stream=None):
+        from paper_2412_20185_b200.layer import _stream_ptr
+
+        self._lib.decdec_stack_launch(self.handle, _stream_ptr(stream))
+
+    def close(self):
+        if self.handle:
+            self._lib.decdec_stack_destroy(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -254,3 +254,91 @@ def test_stack_graph_matches_per_layer_calls():
     for a, b in zip(ys, ref):
         assert torch.equal(a, b)
     st.close()
+
+
+# ------------------------------------------------------------------ TP entry points (1 rank)
+def _comm1():
+    assert dd.decdec_nccl_version() > 0, "NCCL could not be loaded by libdecdec"
+    return dd.decdec_comm_init(dd.decdec_nccl_unique_id(), 0, 1)
+
+
+def test_linear_tp_single_rank_matches_linear():
+    """decdec_linear_tp on a 1-rank library communicator == decdec_linear (the all-gather of one
+    shard is the identity); selection bit-exact against the oracle."""
+    d_in, d_out = 4096, 1024
+    L = gen_perf_layer(d_in, d_out, 3, seed=7)
+    lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"])
+    x = gen_activations(d_in, 1, seed=8)[0]
+    k = oracle.k_from_kchunk(21, d_in)
+    ws = dd.Workspace(k, d_out)
+    comm = _comm1()
+    try:
+        assert dd.decdec_comm_rank(comm) == 0 and dd.decdec_comm_nranks(comm) == 1
+        y_full = torch.empty(d_out, dtype=torch.float16, device=DEV)
+        sel = torch.empty(k, dtype=torch.int32, device=DEV)
+        dd.decdec_linear_tp(lin.struct, to_dev(x).data_ptr(), k, 0, y_full.data_ptr(), sel.data_ptr(),
+                            ws.ptr, ws.nbytes, comm, 0)
+        y_ref = lin(to_dev(x), k, workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(y_full, y_ref)
+        ref = decdec_linear_ref(L["q"], L["s"], L["z"], x, k, rc=L["rc"], rS=L["rS"])
+        assert np.array_equal(sel.cpu().numpy(), ref["idx"])
+        check_close(y_full, ref, "linear_tp")
+    finally:
+        dd.decdec_comm_destroy(comm)
+
+
+def test_stack_tp_single_rank_matches_stack():
+    shapes = [(4096, 1024), (1024, 4096)]
+    lins, xs = [], []
+    for i, (d_in, d_out) in enumerate(shapes):
+        L = gen_perf_layer(d_in, d_out, 3, seed=300 + i)
+        lins.append(dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"]))
+        xs.append(to_dev(gen_activations(d_in, 1, seed=400 + i)[0]))
+    ks = [oracle.k_from_kchunk(21, d_in) for d_in, _ in shapes]
+    ws = dd.Workspace(max(ks), 4096)
+    ref = [lin(x, k, workspace=ws).clone() for lin, x, k in zip(lins, xs, ks)]
+    ys = [torch.empty(d_out, dtype=torch.float16, device=DEV) for _, d_out in shapes]
+    comm = _comm1()
+    try:
+        h = dd.decdec_stack_create_tp([l.struct for l in lins], ks, 0, [x.data_ptr() for x in xs],
+                                      [y.data_ptr() for y in ys], ws.ptr, ws.nbytes, comm, 0)
+        for _ in range(2):
+            dd.decdec_stack_launch(h, 0)
+        torch.cuda.synchronize()
+        for a, b in zip(ys, ref):
+            assert torch.equal(a, b)
+        dd.decdec_stack_destroy(h)
+    finally:
+        dd.decdec_comm_destroy(comm)
+
+
+def test_tp_python_classes_world1():
+    """Comm (unique id over a torch PG) + TPLinear + TPStack on a 1-rank group."""
+    import socket
+
+    import torch.distributed as dist
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        d_in, d_out = 1024, 2048
+        L = gen_perf_layer(d_in, d_out, 4, seed=9)
+        lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 4, rc=L["rc"], rS=L["rS"])
+        x = to_dev(gen_activations(d_in, 1, seed=10)[0])
+        k = oracle.k_from_kchunk(32, d_in)
+        ws = dd.Workspace(k, d_out)
+        comm = dd.Comm()
+        y_ref = lin(x, k, workspace=ws).clone()
+        y_tp = dd.TPLinear(lin, comm)(x, k, workspace=ws)
+        y_st = torch.empty(d_out, dtype=torch.float16, device=DEV)
+        st = dd.TPStack([lin], [k], [x], [y_st], ws, comm)
+        st.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(y_tp, y_ref) and torch.equal(y_st, y_ref)
+        st.close()
+        comm.close()
+    finally:
+        dist.destroy_process_group()

@@ -59,7 +59,11 @@ def _worker(rank, world, port, q):
         dist.all_gather(parts, ys)
         y_full = torch.cat(parts).numpy()
         ref = oracle.decdec_linear_ref(L["q"], L["s"], L["z"], x, k, rc=L["rc"], rS=L["rS"])["y64"]
-        q.put((rank, same, bool(np.array_equal(y_full, ref)), tp.shard_columns(d_out, world)))
+        # the library communicator's NCCL unique id: made on rank 0 only, identical bytes everywhere
+        calls = []
+        uid = tp.broadcast_unique_id(make_id=lambda: calls.append(1) or bytes(range(128)))
+        uid_ok = uid == bytes(range(128)) and len(calls) == (1 if rank == 0 else 0)
+        q.put((rank, same and uid_ok, bool(np.array_equal(y_full, ref)), tp.shard_columns(d_out, world)))
     finally:
         dist.destroy_process_group()
 
@@ -84,6 +88,6 @@ def test_tp_world2_gloo():
     for p in procs:
         p.join(timeout=60)
     for rank, same, equal, cols in res:
-        assert same, f"rank {rank}: selection differs across ranks"
+        assert same, f"rank {rank}: selection or NCCL unique id differs across ranks"
         assert equal, f"rank {rank}: assembled y differs from unsharded oracle"
         assert cols == [(0, 256), (256, 512)]
