@@ -333,6 +333,18 @@ LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, 
     env_prefetch = e ? atoi(e) : 8;
   }
   p.prefetch = env_prefetch;
+  static int env_l2pf = -1;
+  if (env_l2pf < 0) {
+    const char* e = getenv("DECDEC_L2PF");
+    env_l2pf = e ? atoi(e) : 0;
+  }
+  p.l2pf = env_l2pf;
+  static int env_xpf = -1;
+  if (env_xpf < 0) {
+    const char* e = getenv("DECDEC_XPF");
+    env_xpf = e ? atoi(e) : 1;
+  }
+  p.x_pf = env_xpf;
   return p;
 }
 

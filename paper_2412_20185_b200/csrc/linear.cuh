@@ -86,7 +86,9 @@ struct LinearParams {
   // deterministic result in every DEC CTA, no cross-CTA hand-off), keeps S and x[S] in smem and
   // gathers its share of the (segment, row chunk) items.  The other CTAs run the GEMV.
   int n_dec, k_req, chunk;
-  int prefetch;  // weight tiles requested per CTA before griddepcontrol.wait
+  int prefetch;  // weight tiles requested per CTA (into smem) before griddepcontrol.wait
+  int l2pf;      // further tiles per CTA prefetched into L2 only before griddepcontrol.wait
+  int x_pf;      // prefetch x into L2 before griddepcontrol.wait
   int* sel_out;
 };
 
@@ -118,14 +120,24 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   if (split) select_regs_zero(SR);
 #endif
   else if (regs) select_regs_zero(SR);
+  const int nw = blockDim.x >> 5;
+  const int ns = (p.n_seg - (int)blockIdx.x + p.n_dec - 1) / p.n_dec;  // local segments
+  if (RBITS == 4) {
+    // all scale factors are fetched every call; they do not depend on x, so their
+    // zero-copy reads are issued before griddepcontrol.wait (oldest cp.async group: every
+    // later wait_group covers it)
+    for (int i = warp; i < ns; i += nw) {
+      const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
+      if (col0 < p.d_out) cp_async_16(srsc + i * kSegCols + lane * 8, p.r_scales + col0);
+    }
+    cp_async_commit();
+  }
   __syncthreads();
   pdl_wait();  // x may be the previous layer's product; the workspace is the previous layer's
   if (threadIdx.x == 0) {
     DECDEC_TRACE(p, 5);
     if (tr) tr[15] = clock64();  // selection phases 16-19 are SM cycles relative to this
   }
-  const int nw = blockDim.x >> 5;
-  const int ns = (p.n_seg - (int)blockIdx.x + p.n_dec - 1) / p.n_dec;  // local segments
   const int n_items = ns * p.gws;
   using Vec = typename std::conditional<RBITS == 4, uint32_t, uint4>::type;
   constexpr int kGR = RBITS == 4 ? kGatherRows4 : kGatherRows16;
@@ -137,8 +149,6 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     const bool cv = col0 < p.d_out;
     const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
     Vec* dst = stage + bsel * p.rpi * 32 + lane;
-    if (RBITS == 4 && j == 0 && cv)  // all scale factors are fetched every call
-      cp_async_16(srsc + i * kSegCols + lane * 8, p.r_scales + col0);
 #pragma unroll
     for (int r = 0; r < kGR; ++r) {
       const int e = e0 + r;
@@ -259,6 +269,16 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   }
   if (one_seg && had_item) store_part(0, warp, acc);
   if (lane == 0 && (warp == 0 || warp == nw - 1)) DECDEC_TRACE(p, warp == 0 ? 7 : 1);  // gather done
+  // the combine warp of local segment `warp` reads its o_b entries before the barrier: the GEMV
+  // CTAs normally stored them long ago, so the L2 round trip overlaps the slowest warp's gather
+  uint4 ob0 = make_uint4(kObEmpty, kObEmpty, kObEmpty, kObEmpty), ob1 = ob0;
+  {
+    const int col0 = ((int)blockIdx.x + warp * p.n_dec) * kSegCols + lane * 8;
+    if (warp < ns && col0 < p.d_out) {
+      ob0 = ld_relaxed_gpu_u4(p.ob + col0);
+      ob1 = ld_relaxed_gpu_u4(p.ob + col0 + 4);
+    }
+  }
   __syncthreads();  // all partials of the CTA's segments are in smem
   if (threadIdx.x == 0) DECDEC_TRACE(p, 12);
   // ---- step 4: combine, one warp per local segment.  o_b entries are self-validating (relaxed
@@ -267,7 +287,11 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     const int seg = (int)blockIdx.x + i * p.n_dec;
     const int col0 = seg * kSegCols + lane * 8;
     if (col0 < p.d_out) {
-      uint4 o0 = ld_relaxed_gpu_u4(p.ob + col0), o1 = ld_relaxed_gpu_u4(p.ob + col0 + 4);
+      uint4 o0 = ob0, o1 = ob1;
+      if (i != warp) {
+        o0 = ld_relaxed_gpu_u4(p.ob + col0);
+        o1 = ld_relaxed_gpu_u4(p.ob + col0 + 4);
+      }
       while ((o0.x == kObEmpty) | (o0.y == kObEmpty) | (o0.z == kObEmpty) | (o0.w == kObEmpty) |
              (o1.x == kObEmpty) | (o1.y == kObEmpty) | (o1.z == kObEmpty) | (o1.w == kObEmpty)) {
         __nanosleep(32);
@@ -321,6 +345,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
   // streaming their (static) weights while we finish (cross-layer overlap).
   pdl_launch_dependents();
   if (threadIdx.x == 0) DECDEC_TRACE(p, 0);
+  // x into L2 before griddepcontrol.wait (a slice of its 128-B lines per CTA): every CTA's
+  // first loads after the wait -- the selector's and the GEMV's -- then hit L2.  Safe even
+  // while the previous kernel is still producing x: L2 is the coherence point.
+  if (p.x_pf) {
+    const int lines = (p.d_in * 2 + 127) >> 7;
+    const int i = (int)threadIdx.x * 8 + ((int)blockIdx.x & 7);
+    if (i < lines) prefetch_l2(reinterpret_cast<const uint8_t*>(p.x) + ((size_t)i << 7));
+  }
 
   // ------------------------------------------------------------------ DEC CTAs (steps 1-4)
   if ((int)blockIdx.x < p.n_dec) {
@@ -345,6 +377,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       const int stages = p.stages;
       int it = 0, st = 0;
       uint32_t ph = 0;  // phase of the current pass over the ring
+      // L2-only prefetch of the tiles after the smem burst: HBM -> L2 runs while the previous
+      // layer finishes, without queueing ~µs of traffic in front of this SM's x loads
+      for (int i = p.prefetch; i < p.prefetch + p.l2pf; ++i) {
+        const int tile = cta + i * n_cta;
+        if (tile >= p.n_tiles) break;
+        bulk_prefetch_l2(p.w + (size_t)tile * wb, wb);
+      }
       for (int tile = cta; tile < p.n_tiles; tile += n_cta, ++it) {
         // only `prefetch` tiles may be requested before the previous layer completes: a deeper
         // early burst floods the memory pipe and delays the x loads the consumers wait on

@@ -637,10 +637,15 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
     }
     if (tr && lane == 0) tr[11] = clock64();
     const uint32_t ncand = SS->ncand;
+    // x values of the taken candidates come from the keys staged in smem (not a global
+    // round trip on the critical path)
+    const uint16_t* xk_staged = reinterpret_cast<const uint16_t*>(sx);
     if (ncand <= 64u) {
-      select_finish_list<2>(SS, x, ncand, T, need, nD, idx_out, xs_out);
+      select_finish_list<2>(SS, xk_staged, ncand, T, need, nD, idx_out, xs_out);
+    } else if (ncand <= 128u) {  // d-sized inputs: ~70 candidates -> a 128-slot network, not 256
+      select_finish_list<4>(SS, xk_staged, ncand, T, need, nD, idx_out, xs_out);
     } else if (ncand <= (uint32_t)kCandList) {
-      select_finish_list<kCandList / 32>(SS, x, ncand, T, need, nD, idx_out, xs_out);
+      select_finish_list<kCandList / 32>(SS, xk_staged, ncand, T, need, nD, idx_out, xs_out);
     } else {
     const int nwords = (n + 31) >> 5;
     const int W = (nwords + 31) >> 5;  // lane l owns bitmap words [l*W, l*W + W): index order
