@@ -217,6 +217,12 @@ decdec_status decdec_debug_trace(void* buf, size_t bytes);
 /* Launch plan chosen for a layer (tile rows, consumer warps, stages, grid) as text. */
 decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, size_t buf_bytes);
 
+/* Tuning knob (the paper's n_tb; §4.4 tuner): number of DEC CTAs -- CTAs of
+ * the fused layer kernel that select, gather and combine -- used by layer calls planned after
+ * this call (decdec_linear, decdec_stack_create*).  0 (default) = automatic; the plan may
+ * double it when shared memory requires.  1 <= n <= 64.  Process-wide, not thread-safe. */
+decdec_status decdec_set_dec_ctas(int32_t n);
+
 /* Number of kernels decdec_linear enqueues for (k): always 1 (the selector runs on the fused
  * kernel's first CTA(s)). */
 int32_t decdec_launches_per_call(int32_t k);

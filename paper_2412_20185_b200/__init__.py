@@ -30,6 +30,7 @@ from ._lib import (  # noqa: F401
     decdec_pack_weights,
     decdec_plan_string,
     decdec_select,
+    decdec_set_dec_ctas,
     decdec_stack_create,
     decdec_stack_create_tp,
     decdec_stack_destroy,

@@ -61,6 +61,7 @@ def _load():
         "decdec_stack_destroy": (None, [VP]),
         "decdec_status_string": (ctypes.c_char_p, [I32]),
         "decdec_version": (ctypes.c_char_p, []),
+        "decdec_set_dec_ctas": (I32, [I32]),
         "decdec_nccl_version": (I32, []),
         "decdec_nccl_unique_id": (I32, [VP]),
         "decdec_comm_init": (I32, [VP, I32, I32, P(VP)]),
@@ -84,7 +85,7 @@ EXPORTED = [
     "decdec_host_free", "decdec_debug_unpack_weights", "decdec_plan_string", "decdec_launches_per_call",
     "decdec_status_string", "decdec_version", "decdec_stack_create", "decdec_stack_launch",
     "decdec_stack_kernels", "decdec_stack_destroy", "decdec_debug_trace",
-    "decdec_nccl_version", "decdec_nccl_unique_id", "decdec_comm_init", "decdec_comm_destroy",
+    "decdec_set_dec_ctas", "decdec_nccl_version", "decdec_nccl_unique_id", "decdec_comm_init", "decdec_comm_destroy",
     "decdec_comm_rank", "decdec_comm_nranks", "decdec_linear_tp", "decdec_stack_create_tp",
 ]
 
@@ -150,6 +151,10 @@ def decdec_plan_string(L: decdec_layer, k_sel: int) -> str:
     buf = ctypes.create_string_buffer(512)
     _check(_lib.decdec_plan_string(ctypes.byref(L), k_sel, buf, 512), "decdec_plan_string")
     return buf.value.decode()
+
+
+def decdec_set_dec_ctas(n: int):
+    _check(_lib.decdec_set_dec_ctas(n), "decdec_set_dec_ctas")
 
 
 def decdec_launches_per_call(k: int) -> int:

@@ -50,7 +50,10 @@ constexpr size_t kSmemBudget = 200 * 1024;
 // Number of DEC CTAs: ~544 warps of zero-copy reads (measured on the llama3-8b stack at
 // k_chunk 21, 17-warp CTAs: 4 -> 105 us/block, 8 -> 92, 16 -> 84, 32 -> 80, 64 -> 78 within
 // noise, while the GEMV CTAs lose SMs); DECDEC_NDEC overrides.
+int g_dec_override = 0;  // decdec_set_dec_ctas (tuner), 0 = automatic
+
 int dec_ctas(int warps_per_cta) {
+  if (g_dec_override > 0) return g_dec_override;
   static int env = -1;
   if (env < 0) {
     const char* e = getenv("DECDEC_NDEC");
@@ -590,6 +593,12 @@ decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, si
            "\"stages\": %d, \"stage_bytes\": %u, \"n_tiles\": %d, \"grid\": %d, \"threads\": %d, \"smem\": %zu}",
            pl.G, pl.NKW, pl.NSLOTS, pl.RPS, pl.TR, pl.NC, pl.n_dec, pl.stages, pl.stage_bytes, pl.n_tiles, pl.grid,
            32 * (1 + pl.NC), pl.smem);
+  return DECDEC_OK;
+}
+
+decdec_status decdec_set_dec_ctas(int32_t n) {
+  if (n < 0 || n > 64) return DECDEC_EINVAL;
+  g_dec_override = n;
   return DECDEC_OK;
 }
 

@@ -418,7 +418,9 @@ constexpr int kCandList = 256;  // threshold-bin candidates kept as a sortable l
 struct SelectSmemS {
   SelectSmemR r;
   uint32_t bitmap[1024];  // threshold-bin candidates, bit i = key i (n <= 32768)
-  uint32_t cand[kCandList];  // (index << 15 | key) of threshold-bin candidates, arrival order
+  uint32_t cand[kCandList];  // (index << 15 | key) of threshold-bin candidates: warp w's, in index
+                             // order, at [w * cap, w * cap + wcand[w]), cap = kCandList / warps
+  uint32_t wcand[kSelMaxWarps];  // candidates per warp (written by each warp's lane 31)
   uint32_t rest_ready;
   uint32_t ncand;
   uint32_t pad[2];
@@ -570,10 +572,10 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
       const uint32_t u = __shfl_up_sync(0xffffffffu, inc_c, o);
       if (lane >= o) inc_c += u;
     }
-    uint32_t base = 0;
-    if (lane == 31 && inc_c) base = atomicAdd(&SS->ncand, inc_c);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    uint32_t o = base + inc_c - n_c;  // this thread's first list slot
+    // warp-private list region: slots are in index order without any cross-warp allocation
+    const uint32_t cap = (uint32_t)kCandList / (uint32_t)nw;
+    if (lane == 31) SS->wcand[wid] = inc_c;
+    uint32_t o = inc_c - n_c;  // this thread's first slot in its warp's region
     if (n_c) {
 #pragma unroll
       for (int m = 0; m < MAXC; ++m) {
@@ -585,7 +587,7 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
             const uint32_t key = chunk_elem(v[m], jj) & 0x7fffu;
             const uint32_t fb = key & 127u;
             atomicAdd(&S->histB[fb + (fb >> 2)], 1u);
-            if (o < (uint32_t)kCandList) SS->cand[o] = ((uint32_t)(8 * (c0 + m) + jj) << 15) | key;
+            if (o < cap) SS->cand[wid * cap + o] = ((uint32_t)(8 * (c0 + m) + jj) << 15) | key;
           }
         }
       }
@@ -636,16 +638,45 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
       need = (uint32_t)q - nD - above;
     }
     if (tr && lane == 0) tr[11] = clock64();
-    const uint32_t ncand = SS->ncand;
     // x values of the taken candidates come from the keys staged in smem (not a global
     // round trip on the critical path)
     const uint16_t* xk_staged = reinterpret_cast<const uint16_t*>(sx);
-    if (ncand <= 64u) {
-      select_finish_list<2>(SS, xk_staged, ncand, T, need, nD, idx_out, xs_out);
-    } else if (ncand <= 128u) {  // d-sized inputs: ~70 candidates -> a 128-slot network, not 256
-      select_finish_list<4>(SS, xk_staged, ncand, T, need, nD, idx_out, xs_out);
-    } else if (ncand <= (uint32_t)kCandList) {
-      select_finish_list<kCandList / 32>(SS, xk_staged, ncand, T, need, nD, idx_out, xs_out);
+    const uint32_t cap = (uint32_t)kCandList / (uint32_t)nw;
+    const uint32_t wc = lane < nw ? SS->wcand[lane] : 0u;
+    if (!__any_sync(0xffffffffu, wc > cap)) {
+      // warp-ordered lists: lane l walks warp l's candidates (index order), so the lanes'
+      // prefix over (#key > T, #key == T) gives every taken candidate its position directly
+      const uint32_t* L = SS->cand + lane * cap;
+      uint32_t n_gt = 0, n_eq = 0;
+      for (uint32_t i = 0; i < wc; ++i) {
+        const uint32_t key = L[i] & 0x7fffu;
+        n_gt += key > T;
+        n_eq += key == T;
+      }
+      uint32_t inc = (n_eq << 16) | n_gt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      const uint32_t pre = inc - ((n_eq << 16) | n_gt);
+      uint32_t eq_seen = pre >> 16, g_seen = pre & 0xffffu;
+      for (uint32_t i = 0; i < wc; ++i) {
+        const uint32_t v = L[i], key = v & 0x7fffu, ix = v >> 15;
+        if (key > T) {
+          const uint32_t pos = nD + g_seen + min(eq_seen, need);
+          idx_out[pos] = (int)ix;
+          xs_out[pos] = xk_staged[ix];
+          ++g_seen;
+        } else if (key == T) {
+          if (eq_seen < need) {
+            const uint32_t pos = nD + g_seen + eq_seen;
+            idx_out[pos] = (int)ix;
+            xs_out[pos] = xk_staged[ix];
+          }
+          ++eq_seen;
+        }
+      }
     } else {
     const int nwords = (n + 31) >> 5;
     const int W = (nwords + 31) >> 5;  // lane l owns bitmap words [l*W, l*W + W): index order
