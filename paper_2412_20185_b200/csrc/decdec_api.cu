@@ -52,7 +52,11 @@ constexpr size_t kSmemBudget = 200 * 1024;
 // noise, while the GEMV CTAs lose SMs); DECDEC_NDEC overrides.
 int g_dec_override = 0;  // decdec_set_dec_ctas (tuner), 0 = automatic
 
-int dec_ctas(int warps_per_cta) {
+// r = PCIe roofline time / HBM roofline time of the call.  Measured with tools/tune.py on the
+// Llama-3-8B classes (profiles/r01_tuner.json, 17-warp CTAs): while the GEMV bounds the call
+// (r < 1) every SM taken from it costs time and 16 DEC CTAs suffice; once PCIe dominates, more
+// DEC CTAs issue the gather faster (r >= 2.5: 48 beat 32 by 1-3 %).
+int dec_ctas(int warps_per_cta, double r) {
   if (g_dec_override > 0) return g_dec_override;
   static int env = -1;
   if (env < 0) {
@@ -60,15 +64,16 @@ int dec_ctas(int warps_per_cta) {
     env = e ? atoi(e) : 0;
   }
   if (env > 0) return env;
-  int n = (544 + warps_per_cta - 1) / warps_per_cta;
-  return n < 2 ? 2 : (n > 32 ? 32 : n);
+  const int base = r < 1.0 ? 272 : (r < 2.5 ? 544 : 816);  // gather warps
+  int n = (base + warps_per_cta - 1) / warps_per_cta;
+  return n < 2 ? 2 : (n > 48 ? 48 : n);
 }
 
 // DEC CTA layout: CTA c owns segments c, c + n_dec, ...; a segment's k_sel rows are split in
 // gws items of rpi rows, sized so that every warp of a DEC CTA has an item in the first round
 // (items = local segments x gws >= warps) but an item never exceeds one load per row per lane.
 // smem: SelectSmem + staged x | idx, xs | partials [ns][gws][256] f32 | residual scales [ns][256].
-bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, Plan* p) {
+bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, double r, Plan* p) {
   p->n_seg = (d_out + kSegCols - 1) / kSegCols;
   static int env_rpi = -1;
   if (env_rpi < 0) {
@@ -80,7 +85,7 @@ bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, Plan* p
   const uint32_t off_sel = (uint32_t)align_up(sel_bytes, 16);
   const uint32_t off_part = (uint32_t)align_up((size_t)off_sel + (size_t)k_sel * 6, 16);
   const size_t row_b = max_rpi == kGatherRows16 ? 16 : 4;  // bytes per lane per staged row
-  for (int nd = dec_ctas(warps); nd <= 64; nd *= 2) {
+  for (int nd = dec_ctas(warps, r); nd <= 96; nd *= 2) {
     const int ns = (p->n_seg + nd - 1) / nd;
     const int gws_target = (warps + ns - 1) / ns;
     // staging rows per buffer: as many as fit (<= max_rpi); fewer rows -> more, smaller items
@@ -126,6 +131,10 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
     env_rps = 0;
     if (e) sscanf(e, "%d,%d", &env_nc, &env_rps);
   }
+  // PCIe / HBM roofline time ratio with the measured link and copy bandwidths
+  const double t_hbm = ((double)d_in * d_out * bits / 8 + 3.0 * d_out * G) / 6455.0;
+  const double t_pcie = ((double)k_sel * d_out * r_bits / 8 + 2.0 * d_out) / 51.4;
+  const double r_ratio = t_pcie / t_hbm;
   Plan best{};
   double best_cost = 1e300;
   bool have = false;
@@ -168,7 +177,8 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
       p.off_x = (uint32_t)align_up((size_t)p.stages * p.stage_bytes + red + (size_t)2 * p.stages * 8, 16);
       p.smem = p.off_x + xb;
       p.n_dec = 0;
-      if (k_sel > 0 && !plan_dec(d_out, k_sel, sel_len, 1 + nc, r_bits == 16 ? kGatherRows16 : kGatherRows4, &p)) continue;
+      if (k_sel > 0 && !plan_dec(d_out, k_sel, sel_len, 1 + nc, r_bits == 16 ? kGatherRows16 : kGatherRows4, r_ratio, &p))
+        continue;
       const int max_grid = sms - p.n_dec;
       p.grid = p.n_tiles < max_grid ? p.n_tiles : max_grid;
       if (p.smem > kSmemBudget + 16 * 1024) continue;
