@@ -565,13 +565,16 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
       n_c += __popc(cmask[m]);
     }
   }
-  {
-    uint32_t inc_c = n_c;
+  // one lane scan for both counts (a warp holds <= 2048 keys: 16-bit fields)
+  uint32_t inc_cd = (n_c << 16) | n_d;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, inc_c, o);
-      if (lane >= o) inc_c += u;
-    }
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc_cd, o);
+    if (lane >= o) inc_cd += u;
+  }
+  const uint32_t inc_d = inc_cd & 0xffffu;
+  {
+    const uint32_t inc_c = inc_cd >> 16;
     // warp-private list region: slots are in index order without any cross-warp allocation
     const uint32_t cap = (uint32_t)kCandList / (uint32_t)nw;
     if (lane == 31) SS->wcand[wid] = inc_c;
@@ -593,12 +596,6 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
       }
     }
   }
-  uint32_t inc_d = n_d;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t u = __shfl_up_sync(0xffffffffu, inc_d, o);
-    if (lane >= o) inc_d += u;
-  }
   if (lane == 31) S->wsum[wid] = inc_d;
   __syncthreads();  // barrier 2: histB, bitmap, D warp totals complete
   uint32_t pre_d;
@@ -610,7 +607,8 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
       const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
       if (lane >= o) wi += u;
     }
-    pre_d = __shfl_sync(0xffffffffu, wi - wt, wid) + inc_d - n_d;
+    const uint32_t wpre = __shfl_sync(0xffffffffu, wi - wt, wid);
+    pre_d = wpre + inc_d - n_d;
   }
   if (n_d) {  // place D at [0, nD), ascending (only the few threads holding D keys)
     int pos = (int)pre_d;
@@ -857,7 +855,8 @@ __device__ __forceinline__ int select_split_bar(const uint16_t* __restrict__ x, 
       const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
       if (lane >= o) wi += u;
     }
-    pre_d = __shfl_sync(0xffffffffu, wi - wt, wid) + inc_d - n_d;
+    const uint32_t wpre = __shfl_sync(0xffffffffu, wi - wt, wid);
+    pre_d = wpre + inc_d - n_d;
   }
   if (n_d) {
     int pos = (int)pre_d;
