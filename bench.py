@@ -40,6 +40,19 @@ METRIC = "µs per decode linear layer & tokens/s vs k_chunk; % of HBM+PCIe roofl
 GROUP = 128
 
 
+# The paper's own end-to-end results (Table 2): tuner output
+# n_max / (k_qkv, k_o, k_gu, k_d) -> measured slowdown vs the uncompensated model, Llama-3-8B-Instruct
+# 3-bit AWQ, per-token latency in a torch.compile pipeline.  Other hardware: context, not a target.
+PAPER_SLOWDOWNS = {
+    "source": "PAPER.md Table 2 (P:514-554), Llama-3-8B 3-bit AWQ, n_max/(k_qkv,k_o,k_gu,k_d) -> slowdown",
+    "RTX 4090 (1008 GB/s HBM, 32 GB/s PCIe)": {"2.5%": "24/(4,4,8,9) -> 1.3%", "5%": "24/(5,7,9,10) -> 2.2%",
+                                               "10%": "24/(10,11,11,11) -> 4.9%", "20%": "24/(15,15,16,15) -> 10.4%"},
+    "RTX 4050 Mobile (192 GB/s, 16 GB/s PCIe)": {"2.5%": "8/(55,56,58,55) -> 1.7%", "5%": "8/(59,59,59,58) -> 3.3%",
+                                                 "10%": "10/(62,62,62,62) -> 6.6%", "20%": "10/(70,70,68,68) -> 13.5%"},
+    "this B200 (tools/tune.py)": "profiles/r01_tuner.json",
+}
+
+
 def k_of(kc: int, d_in: int) -> int:
     return (kc * d_in) // 1024  # ledger L3: k = floor(k_chunk * d_in / 1024)
 
@@ -464,6 +477,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": kernels_head * args.steps,
             "clocks": clocks,
+            "paper_context": PAPER_SLOWDOWNS,
             "sweep": {str(k): {"tokens_per_s": round(v["tokens_per_s"], 2), "ms_per_step": round(v["ms_per_step"], 4),
                                "slowdown_vs_k0": round(v["ms_per_step"] / results[0]["ms_per_step"], 4)
                                if 0 in results else None}

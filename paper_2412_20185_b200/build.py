@@ -1,4 +1,5 @@
-"""Build libdecdec.so (sm_100a) in-tree with nvcc.  `python -m paper_2412_20185_b200.build`."""
+"""Build libdecdec.so (sm_100a) in-tree with nvcc.  `python paper_2412_20185_b200/build.py` (running it as
+`-m paper_2412_20185_b200.build` would import the package, i.e. load the old library, first)."""
 
 from __future__ import annotations
 

@@ -55,7 +55,8 @@ int g_dec_override = 0;  // decdec_set_dec_ctas (tuner), 0 = automatic
 // r = PCIe roofline time / HBM roofline time of the call.  Measured with tools/tune.py on the
 // Llama-3-8B classes (profiles/r01_tuner.json, 17-warp CTAs): while the GEMV bounds the call
 // (r < 1) every SM taken from it costs time and 16 DEC CTAs suffice; once PCIe dominates, more
-// DEC CTAs issue the gather faster (r >= 2.5: 48 beat 32 by 1-3 %).
+// DEC CTAs issue the gather faster (r >= 2.5: 48 beat 32 by 1-3 %, 64 beat 48 by ~1 % on the
+// k_chunk 21 step).
 int dec_ctas(int warps_per_cta, double r) {
   if (g_dec_override > 0) return g_dec_override;
   static int env = -1;
@@ -64,9 +65,9 @@ int dec_ctas(int warps_per_cta, double r) {
     env = e ? atoi(e) : 0;
   }
   if (env > 0) return env;
-  const int base = r < 1.0 ? 272 : (r < 2.5 ? 544 : 816);  // gather warps
+  const int base = r < 1.0 ? 272 : (r < 2.5 ? 544 : 1088);  // gather warps
   int n = (base + warps_per_cta - 1) / warps_per_cta;
-  return n < 2 ? 2 : (n > 48 ? 48 : n);
+  return n < 2 ? 2 : (n > 64 ? 64 : n);
 }
 
 // DEC CTA layout: CTA c owns segments c, c + n_dec, ...; a segment's k_sel rows are split in

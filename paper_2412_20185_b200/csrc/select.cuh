@@ -22,6 +22,8 @@
 namespace decdec {
 
 constexpr int kSelMaxWarps = 32;
+constexpr int kHistACopies = 4;            // coarse histogram copies (lane & 3); 8 copies measured slower
+constexpr int kHistAStride = 256 + 32 + 8;  // = 8 mod 32: the copies start 8 banks apart
 
 // shared scratch of select_block (plus the staged x: 2 * roundup(len, 8) bytes after it)
 struct SelectSmem {
@@ -221,13 +223,16 @@ __device__ __forceinline__ void select_block(const uint16_t* __restrict__ x, int
 // griddepcontrol.wait); each call leaves S zeroed again after its last barrier... except for
 // the final zeroing, which the caller's barrier after the call orders before the next call.
 struct SelectSmemR {
-  uint32_t histA[4][256 + 32];  // copy c, bin b at b + (b >> 3)
+  // copy c, bin b at b + (b >> 3).  Activation magnitudes crowd a few bins, so lanes sharing a
+  // copy often hit the same address (serialised atomics): 4 copies, on distinct bank offsets
+  // (8 copies: the bin scan's extra reads cost more than the conflicts they save)
+  uint32_t histA[kHistACopies][kHistAStride];
   uint32_t histB[128 + 32];     // bin b at b + (b >> 2)
   uint32_t wsum[kSelMaxWarps];  // per-warp (n_eq << 16 | n_gt) totals
 };
 __device__ __forceinline__ void select_regs_zero(SelectSmemR* S) {
   uint32_t* h = &S->histA[0][0];
-  for (int i = threadIdx.x; i < 4 * (256 + 32) + 128 + 32; i += blockDim.x) h[i] = 0u;
+  for (int i = threadIdx.x; i < kHistACopies * kHistAStride + 128 + 32; i += blockDim.x) h[i] = 0u;
 }
 
 // warp-redundant version of warp_find_bin: every lane gets (bin, above) for the q-th largest
@@ -285,7 +290,7 @@ __device__ __forceinline__ void select_block_regs(const uint16_t* __restrict__ x
   for (int m = 0; m < MAXC; ++m) v[m] = m < nv ? __ldg(x4 + m) : make_uint4(0, 0, 0, 0);
   SEL_TRACE(16);
   // ---- coarse histogram (key >> 7), 4 copies
-  uint32_t* hA = S->histA[lane & 3];
+  uint32_t* hA = S->histA[lane & (kHistACopies - 1)];
 #pragma unroll
   for (int m = 0; m < MAXC; ++m) {
     if (m < nv) {
@@ -369,7 +374,7 @@ __device__ __forceinline__ void select_block_regs(const uint16_t* __restrict__ x
   SEL_TRACE(19);
   {  // zero the histograms for the next call (the caller's barrier orders it before that call)
     uint32_t* h = &S->histA[0][0];
-    for (int i = t; i < 4 * (256 + 32) + 128 + 32; i += NT) h[i] = 0u;
+    for (int i = t; i < kHistACopies * kHistAStride + 128 + 32; i += NT) h[i] = 0u;
   }
   const uint32_t pre = wpre + inc - mine;
   if (n_gt + n_eq) {
@@ -523,7 +528,7 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
   SEL_TRACE(16);
   uint4* sx = reinterpret_cast<uint4*>(SS + 1);  // staged keys for the finisher warp
   // ---- coarse histogram (key >> 7), 4 copies
-  uint32_t* hA = S->histA[lane & 3];
+  uint32_t* hA = S->histA[lane & (kHistACopies - 1)];
 #pragma unroll
   for (int m = 0; m < MAXC; ++m) {
     if (m < nv) {
@@ -801,7 +806,7 @@ __device__ __forceinline__ int select_split_bar(const uint16_t* __restrict__ x, 
 #pragma unroll
   for (int m = 0; m < MAXC; ++m) v[m] = m < nv ? __ldg(x4 + m) : make_uint4(0, 0, 0, 0);
   SEL_TRACE(16);
-  uint32_t* hA = S->histA[lane & 3];
+  uint32_t* hA = S->histA[lane & (kHistACopies - 1)];
 #pragma unroll
   for (int m = 0; m < MAXC; ++m) {
     if (m < nv) {
