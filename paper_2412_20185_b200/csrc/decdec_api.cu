@@ -99,7 +99,8 @@ bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, double 
       const int one_seg = ns == 1;
       const int nparts = one_seg ? (gws < warps ? gws : warps) : gws;
       const uint32_t off_rsc = off_part + (uint32_t)ns * nparts * kSegCols * 4;
-      const uint32_t off_stage = (uint32_t)align_up((size_t)off_rsc + (size_t)ns * kSegCols * 2, 16);
+      // + 16 B: the mbarrier the residual scales' bulk copies complete on
+      const uint32_t off_stage = (uint32_t)align_up((size_t)off_rsc + (size_t)ns * kSegCols * 2 + 16, 16);
       const size_t dec = off_stage + (size_t)warps * 2 * rpi * 32 * row_b;
       if (dec > kSmemBudget + 16 * 1024) continue;
       p->n_dec = nd;

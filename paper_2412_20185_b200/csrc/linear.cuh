@@ -122,15 +122,25 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   else if (regs) select_regs_zero(SR);
   const int nw = blockDim.x >> 5;
   const int ns = (p.n_seg - (int)blockIdx.x + p.n_dec - 1) / p.n_dec;  // local segments
-  if (RBITS == 4) {
-    // all scale factors are fetched every call; they do not depend on x, so their
-    // zero-copy reads are issued before griddepcontrol.wait (oldest cp.async group: every
-    // later wait_group covers it)
-    for (int i = warp; i < ns; i += nw) {
-      const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
-      if (col0 < p.d_out) cp_async_16(srsc + i * kSegCols + lane * 8, p.r_scales + col0);
+  uint64_t* scale_bar = reinterpret_cast<uint64_t*>(srsc + ns * kSegCols);
+  if (RBITS == 4 && threadIdx.x == 0) {
+    // all scale factors are fetched every call; they do not depend on x, so they are
+    // requested before griddepcontrol.wait, as one bulk copy (TMA) per segment: exactly the
+    // segment's bytes cross PCIe (16-B cp.async per lane read every 32-B sector twice, ncu),
+    // and no LSU work; the combine waits on scale_bar
+    mbar_init(scale_bar, 1);
+    fence_mbar_init();
+    uint32_t bytes = 0;
+    for (int i = 0; i < ns; ++i) {
+      const int c = ((int)blockIdx.x + i * p.n_dec) * kSegCols;
+      if (c < p.d_out) bytes += (uint32_t)min(kSegCols, p.d_out - c) * 2;
     }
-    cp_async_commit();
+    mbar_arrive_expect_tx(scale_bar, bytes);
+    const uint64_t pol = policy_evict_first();
+    for (int i = 0; i < ns; ++i) {
+      const int c = ((int)blockIdx.x + i * p.n_dec) * kSegCols;
+      if (c < p.d_out) bulk_g2s(srsc + i * kSegCols, p.r_scales + c, (uint32_t)min(kSegCols, p.d_out - c) * 2, scale_bar, pol);
+    }
   }
   __syncthreads();
   pdl_wait();  // x may be the previous layer's product; the workspace is the previous layer's
@@ -280,6 +290,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     }
   }
   __syncthreads();  // all partials of the CTA's segments are in smem
+  if (RBITS == 4 && warp < ns) mbar_wait(scale_bar, 0);  // the scales' bulk copies landed
   if (threadIdx.x == 0) DECDEC_TRACE(p, 12);
   // ---- step 4: combine, one warp per local segment.  o_b entries are self-validating (relaxed
   // stores of the GEMV CTAs, kObEmpty until written): poll them, then restore kObEmpty.

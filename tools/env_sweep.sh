@@ -4,7 +4,7 @@
 out=${OUT:-gpurun_out/env_sweep.txt}
 : > "$out"
 for setting in "$@"; do
-  line=$(env $setting timeout 300 python bench.py --sweep-only --steps ${STEPS:-30} --warmup 5 \
+  line=$(env $setting timeout 300 python bench.py ${BENCH_ARGS:-} --sweep-only --steps ${STEPS:-30} --warmup 5 \
          --sweep ${SWEEP:-0,21} 2>/dev/null | tail -1)
   python - "$setting" "$line" >> "$out" <<'PY'
 import json, sys
