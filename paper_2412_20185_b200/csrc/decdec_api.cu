@@ -525,6 +525,18 @@ decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const i
     delete[] P;
     return cuda_status(e0);
   }
+  if (gather) {
+    // NCCL sets up connections / algorithm buffers lazily on a communicator's first
+    // collectives: run each layer's all-gather once outside the capture (in place on y_full,
+    // whose contents are overwritten by every replay anyway)
+    for (int i = 0; i < n_layers && s == DECDEC_OK; ++i) s = tp_allgather(comm, y[i], layers[i].d_out, st);
+    if (s == DECDEC_OK) s = cuda_status(cudaStreamSynchronize(st));
+    if (s != DECDEC_OK) {
+      cudaStreamDestroy(st);
+      delete[] P;
+      return s;
+    }
+  }
   decdec_stack* g = new decdec_stack();
   cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
   for (int i = 0; i < n_layers && e == cudaSuccess && s == DECDEC_OK; ++i) {

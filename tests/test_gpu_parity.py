@@ -342,3 +342,52 @@ def test_tp_python_classes_world1():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_validation_error_codes():
+    """include/decdec.h error contract: synchronous validation, nothing enqueued, the documented
+    status per violated condition."""
+    import ctypes
+
+    L = gen_perf_layer(1024, 256, 3, seed=5)
+    lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"])
+    ws = dd.Workspace(64, 256)
+    x = to_dev(gen_activations(1024, 1, seed=6)[0])
+    y = torch.empty(256, dtype=torch.float16, device=DEV)
+    s = torch.cuda.current_stream().cuda_stream
+
+    def call(st, k=16, chunk=0, xp=None, yp=None, wsp=None, wsb=None):
+        try:
+            dd.decdec_linear(st, x.data_ptr() if xp is None else xp, k, chunk, y.data_ptr() if yp is None else yp,
+                             0, ws.ptr if wsp is None else wsp, ws.nbytes if wsb is None else wsb, s)
+            return 0
+        except dd.DecdecError as e:
+            return e.status
+
+    def mod(**kw):
+        st = dd.decdec_layer()
+        ctypes.pointer(st)[0] = lin.struct
+        for k, v in kw.items():
+            setattr(st, k, v)
+        return st
+
+    base = lin.struct
+    assert call(base) == 0
+    assert call(mod(group_size=64)) == -4          # EUNSUPPORTED
+    assert call(mod(w_bits=5)) == -4
+    assert call(mod(r_bits=8)) == -4
+    assert call(mod(d_in=1000)) == -1              # EINVAL: d_in % 128
+    assert call(mod(d_out=100)) == -1              # d_out % 32
+    assert call(mod(w_packed=base.w_packed + 4)) == -2   # EALIGN
+    assert call(mod(r_scales=None)) == -1
+    assert call(base, k=1025) == -1                # k > d_in
+    assert call(base, k=-1) == -1
+    assert call(base, chunk=1024, k=2000) == -1    # k_chunk > chunk
+    assert call(base, xp=0) == -1                  # NULL x
+    assert call(base, yp=y.data_ptr() + 2) == -2   # misaligned y
+    assert call(base, wsb=16) == -7                # ESPACE
+    torch.cuda.synchronize()
+    with pytest.raises(dd.DecdecError):
+        dd.decdec_linear_tp(base, x.data_ptr(), 16, 0, y.data_ptr(), 0, ws.ptr, ws.nbytes, 0, s)  # NULL comm
+    with pytest.raises(dd.DecdecError):
+        dd.decdec_set_dec_ctas(65)
