@@ -302,6 +302,9 @@ def main():
     ap.add_argument("--nx", type=int, default=4, help="distinct activation sets cycled across steps")
     ap.add_argument("--quick", action="store_true", help="headline step only (for ncu launch lists)")
     ap.add_argument("--sweep-only", action="store_true", help="decode-step sweep only (no per-shape table, no oracle)")
+    ap.add_argument("--shard-of", type=int, default=1,
+                    help="single GPU: run rank 0's output-feature shard of a P-way TP model (d_out/P per layer, "
+                         "its own host residual slice); per-rank time, all-gather NOT included (config 4/5 evidence)")
     ap.add_argument("--unfused", action="store_true",
                     help="7 separate q/k/v/o/gate/up/down calls per block instead of the paper's layer "
                          "classes qkv, o, gu, d (P:304); per-layer µs of the 7 shapes are reported either way")
@@ -327,7 +330,8 @@ def main():
     hbm_peak, hbm_src, pcie_peak, pcie_src = load_peaks()
 
     t_build = time.time()
-    M = Model(dd, torch, args.model, args.bits, rank, world, args.nx, dev, fused=not args.unfused)
+    shard = world if world > 1 else max(1, args.shard_of)
+    M = Model(dd, torch, args.model, args.bits, rank, shard, args.nx, dev, fused=not args.unfused)
     sweep = sorted({int(v) for v in args.sweep.split(",") if v != ""} | {args.kchunk})
     if args.quick:
         sweep, args.no_cpu_baseline = [args.kchunk], True
@@ -469,7 +473,9 @@ def main():
                                    f"{M.n_blocks} blocks, w{args.bits} g128, r4 residual in pinned host memory, "
                                    f"exact Top-k, k_chunk={args.kchunk}",
                        "k_chunk": args.kchunk, "layers_per_step": n_layers,
-                       "parallelism": f"tp{world} (output-feature shards + NCCL all-gather)" if world > 1 else "single GPU",
+                       "parallelism": (f"tp{world} (output-feature shards + NCCL all-gather)" if world > 1 else
+                                       f"single GPU running rank 0's 1/{shard} output-feature shard (all-gather not included)"
+                                       if shard > 1 else "single GPU"),
                        "l2": f"inputs larger than L2: {step_hbm / 1e9:.2f} GB weights streamed per step",
                        "x_sets": args.nx},
             "roofline": roofline,
