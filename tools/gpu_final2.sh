@@ -1,3 +1,4 @@
+# Secondary bench lines: 4-bit (config 3), Phi-3 (config 4), rank 0 of 8 for 70B / Phi-3 (configs 4/5)
 timeout 900 python bench.py --bits 4 --no-cpu-baseline > gpurun_out/final_bench_w4.json 2> /dev/null
 timeout 900 python bench.py --model phi3_medium --no-cpu-baseline --sweep 0,21 > gpurun_out/final_bench_phi3.json 2> /dev/null
 timeout 1200 python bench.py --model llama3_70b --shard-of 8 --no-cpu-baseline --sweep 0,21 --steps 50 > gpurun_out/final_bench_70b_shard8.json 2> /dev/null
