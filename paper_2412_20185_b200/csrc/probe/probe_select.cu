@@ -53,6 +53,14 @@ int main() {
       CK(cudaFuncSetAttribute(k_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       k_sel<<<1, nt, sm>>>(dx, n, q, iters, didx, dxs, dtr);
       CK(cudaDeviceSynchronize());
+      {  // result checksum (order-sensitive) to compare selector variants
+        int* hi = (int*)malloc(q * 4);
+        CK(cudaMemcpy(hi, didx, q * 4, cudaMemcpyDeviceToHost));
+        unsigned long long cs = 0;
+        for (int i = 0; i < q; ++i) cs = cs * 1000003ull + (unsigned)hi[i];
+        printf("checksum n=%d threads=%d: %llu\n", n, nt, cs);
+        free(hi);
+      }
       static unsigned long long h[1000 * 20];
       CK(cudaMemcpy(h, dtr, iters * 20 * 8, cudaMemcpyDeviceToHost));
       for (int it : {0, 1, iters - 1}) {
