@@ -460,6 +460,22 @@ def main():
                "sample": f"one decoder block ({', '.join(times)}) through oracle.decdec_linear_ref at "
                          f"k_chunk={args.kchunk}, x {M.n_blocks} blocks; {blk:.1f} s of CPU work",
                "per_layer_s": {k: round(v, 3) for k, v in times.items()}}
+        # also one thread, and the host it ran on
+        try:
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                t1 = cpu_oracle_block(args.model, args.bits, args.kchunk, fused=not args.unfused)
+            cpu["value_1thread"] = 1.0 / (M.n_blocks * sum(t1.values()))
+        except Exception as e:  # threadpoolctl missing: report why
+            cpu["value_1thread"] = None
+            cpu["value_1thread_error"] = str(e)[:120]
+        cpu["affinity_cpus"] = len(os.sched_getaffinity(0))
+        try:
+            info = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+            get = lambda key: next((ln.split(":", 1)[1].strip() for ln in info.splitlines() if ln.startswith(key)), None)  # noqa: E731
+            cpu["host_cpu"] = {"model": get("Model name"), "sockets": get("Socket(s)")}
+        except Exception:
+            pass
 
     if rank == 0:
         line = {
