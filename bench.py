@@ -377,7 +377,7 @@ def main():
         if name not in shape_names:
             shape_names.append(name)
     per_shape = {}
-    if world == 1 and not (args.quick or args.sweep_only):
+    if not (args.quick or args.sweep_only):  # per rank under TP: the rank's shards, no collective
         for name in shape_names:
             idx = [i for i, m in enumerate(M.meta) if m[1] == name]
             d_in, d_out = M.meta[idx[0]][2], M.meta[idx[0]][3]
@@ -387,7 +387,7 @@ def main():
                 xs = [M.xs(s) for s in range(args.nx)]
                 stacks = [dd.Stack(lay, M.ks(kc, idx), [xs[s][i] for i in idx], [M.ys()[i] for i in idx], ws)
                           for s in range(args.nx)]
-                ms = time_graphs(torch, dist, [st.launch for st in stacks], max(8, args.steps // 4), 3, stream, 1)
+                ms = time_graphs(torch, dist, [st.launch for st in stacks], max(8, args.steps // 4), 3, stream, world)  # max over ranks
                 us = 1e3 * ms / len(idx)
                 k = k_of(kc, d_in)
                 bh, bp = bytes_hbm(d_in, d_out, args.bits), bytes_pcie(k, d_out)
@@ -435,11 +435,12 @@ def main():
         ach = (bp if pcie_bound else bh) / e["us"] / 1e3
         peak = pcie_peak if pcie_bound else hbm_peak
         traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
-                traffic = json.load(f).get(f"{dom}/{args.kchunk}")
-        except Exception:
-            pass
+        if shard == 1 and args.model == "llama3_8b" and args.bits == 3:  # the captured layer's shape only
+            try:
+                with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+                    traffic = json.load(f).get(f"{dom}/{args.kchunk}")
+            except Exception:
+                pass
         roofline = {
             "bound": "pcie" if pcie_bound else "hbm", "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
             "frac": round(ach / peak, 4), "traffic": traffic,
