@@ -136,10 +136,13 @@ class ClockSampler:
 class Model:
     """Llama-3-8B (or another model) decode linear stack on this rank."""
 
-    def __init__(self, dd, torch, model, bits, rank, world, n_x_sets, device, fused=True):
+    def __init__(self, dd, torch, model, bits, rank, world, n_x_sets, device, fused=True, hosts=None, numa=-1,
+                 shapes=None):
+        """hosts: reuse another Model's host residual store (same shapes; the residual does not
+        depend on the base bit width).  numa: NUMA node of the rank's residual slice."""
         self.layers, self.meta = [], []  # meta: (block, name, d_in, d_out_shard)
         self.hosts = []
-        shapes = model_layers(model, fused=fused)
+        shapes = model_layers(model, fused=fused) if shapes is None else shapes
         self.n_blocks = MODEL_BLOCKS[model]
         for b in range(self.n_blocks):
             for name, d_in, d_out in shapes:
@@ -148,10 +151,13 @@ class Model:
                                                               device=device)
                 row_bytes = d_out_r // 2
                 sc_off = (d_in * row_bytes + 255) // 256 * 256
-                hb = dd.HostBuffer(sc_off + 2 * d_out_r)
-                hv = torch.from_numpy(hb.numpy(np.uint8))
-                hv[: d_in * row_bytes].copy_(g["r"].cpu())
-                hv[sc_off: sc_off + 2 * d_out_r].copy_(g["rS"].view(torch.uint8).cpu())
+                if hosts is not None:
+                    hb = hosts[len(self.hosts)]
+                else:
+                    hb = dd.HostBuffer(sc_off + 2 * d_out_r, numa)
+                    hv = torch.from_numpy(hb.numpy(np.uint8))
+                    hv[: d_in * row_bytes].copy_(g["r"].cpu())
+                    hv[sc_off: sc_off + 2 * d_out_r].copy_(g["rS"].view(torch.uint8).cpu())
                 del g["r"]
                 lin = dd.QuantLinear.from_device_packed(d_in, d_out_r, bits, g["w"], g["s"], g["z"], host=hb,
                                                         r_bits=4, host_scales_off=sc_off)
@@ -205,6 +211,66 @@ def time_graphs(torch, dist, launches, K, W, stream, world):
         ms = float(t.item())
         dist.barrier()
     return ms
+
+
+def time_shapes(torch, dist, dd, M, ws, sweep, steps, stream, world, bits, hbm_peak, pcie_peak, names=None):
+    """µs per layer call of each shape: a graph of the model's n_blocks instances of that shape
+    (distinct weights, PDL-chained), per k_chunk; with HBM/PCIe achieved GB/s and roofline fraction."""
+    shape_names = []
+    for (_, name, _, _) in M.meta:
+        if name not in shape_names and (names is None or name in names):
+            shape_names.append(name)
+    per_shape = {}
+    for name in shape_names:
+        idx = [i for i, m in enumerate(M.meta) if m[1] == name]
+        d_in, d_out = M.meta[idx[0]][2], M.meta[idx[0]][3]
+        per_shape[name] = {"d_in": d_in, "d_out": d_out}
+        for kc in sweep:
+            lay = [M.layers[i] for i in idx]
+            xs = [M.xs(s) for s in range(len(M.x_dev))]
+            stacks = [dd.Stack(lay, M.ks(kc, idx), [xs[s][i] for i in idx], [M.ys()[i] for i in idx], ws)
+                      for s in range(len(M.x_dev))]
+            ms = time_graphs(torch, dist, [st.launch for st in stacks], max(8, steps // 4), 3, stream, world)
+            us = 1e3 * ms / len(idx)
+            k = k_of(kc, d_in)
+            bh, bp = bytes_hbm(d_in, d_out, bits), bytes_pcie(k, d_out)
+            t_roof = max(bh / (hbm_peak * 1e3), bp / (pcie_peak * 1e3))  # µs
+            per_shape[name][str(kc)] = {"us": round(us, 3), "k": k, "hbm_GBps": round(bh / us / 1e3, 1),
+                                        "pcie_GBps": round(bp / us / 1e3, 2), "roofline_us": round(t_roof, 3),
+                                        "roofline_frac": round(t_roof / us, 3),
+                                        "hbm_frac": round(bh / us / 1e3 / hbm_peak, 3)}
+            for st in stacks:
+                st.close()
+    return per_shape
+
+
+def step_sweep(torch, dist, dd, M, ws, sweep, steps, warmup, stream, world, comm=None):
+    """tokens/s of the whole decode step (all layers, one CUDA graph per activation set) per k_chunk."""
+    out = {}
+    for kc in sweep:
+        if comm is None:
+            stacks = [dd.Stack(M.layers, M.ks(kc), M.xs(s), M.ys(), ws) for s in range(len(M.x_dev))]
+        else:
+            full = [torch.empty(m[3] * world, dtype=torch.float16, device="cuda") for m in M.meta]
+            stacks = [dd.TPStack(M.layers, M.ks(kc), M.xs(s), full, ws, comm) for s in range(len(M.x_dev))]
+        ms = time_graphs(torch, dist, [st.launch for st in stacks], steps, max(warmup, 3), stream, world)
+        out[kc] = {"ms_per_step": ms, "tokens_per_s": 1e3 / ms, "kernels_per_step": stacks[0].kernels}
+        for st in stacks:
+            st.close()
+    return out
+
+
+def knee(results, bits, hbm_peak, pcie_peak, limit=1.10):
+    """Measured knee: the largest swept k_chunk whose step time is <= limit x the k_chunk-0 step,
+    next to the paper's prediction k_chunk = 1024 / R_bw * b / 4 (R_bw = HBM / PCIe BW)."""
+    if 0 not in results:
+        return None
+    base = results[0]["ms_per_step"]
+    ok = [kc for kc in sorted(results) if results[kc]["ms_per_step"] <= limit * base]
+    r_bw = hbm_peak / pcie_peak
+    return {"limit": limit, "measured_k_chunk": max(ok) if ok else 0,
+            "predicted_k_chunk_P384": round(1024.0 / r_bw * bits / 4.0, 2), "R_bw": round(r_bw, 1),
+            "note": "paper knee formula (P:384) with the measured HBM copy and zero-copy PCIe bandwidths"}
 
 
 def cpu_oracle_block(model, bits, kc, fused=True, seed_tag="cpu"):
@@ -297,7 +363,8 @@ def main():
     ap.add_argument("--model", default="llama3_8b")
     ap.add_argument("--bits", type=int, default=3)
     ap.add_argument("--kchunk", type=int, default=21, help="headline k_chunk (21 = 2.05%% of channels)")
-    ap.add_argument("--sweep", default="0,4,8,16,21,32", help="k_chunk sweep (µs/layer per shape + tokens/s)")
+    ap.add_argument("--sweep", default="0,1,2,4,6,8,12,16,21,32,48,64,82",
+                    help="k_chunk sweep (µs/layer per shape + tokens/s); SURVEY §8(d) config 2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nx", type=int, default=4, help="distinct activation sets cycled across steps")
     ap.add_argument("--quick", action="store_true", help="headline step only (for ncu launch lists)")
@@ -307,7 +374,11 @@ def main():
                          "its own host residual slice); per-rank time, all-gather NOT included (config 4/5 evidence)")
     ap.add_argument("--unfused", action="store_true",
                     help="7 separate q/k/v/o/gate/up/down calls per block instead of the paper's layer "
-                         "classes qkv, o, gu, d (P:304); per-layer µs of the 7 shapes are reported either way")
+                         "classes qkv, o, gu, d (P:304).  Without it the per-layer table still carries the 7 "
+                         "unfused shapes (per_layer_us_unfused: k/v and gate/up timed on their own instances, "
+                         "q = o and down = d shapes)")
+    ap.add_argument("--no-w4", action="store_true", help="skip the 4-bit (config 3) sub-object")
+    ap.add_argument("--no-unfused-extra", action="store_true", help="skip timing the k/v and gate/up shapes")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -331,7 +402,8 @@ def main():
 
     t_build = time.time()
     shard = world if world > 1 else max(1, args.shard_of)
-    M = Model(dd, torch, args.model, args.bits, rank, shard, args.nx, dev, fused=not args.unfused)
+    numa = dd.numa_node_of_device(local)  # the rank's residual slice sits in front of its own PCIe link
+    M = Model(dd, torch, args.model, args.bits, rank, shard, args.nx, dev, fused=not args.unfused, numa=numa)
     sweep = sorted({int(v) for v in args.sweep.split(",") if v != ""} | {args.kchunk})
     if args.quick:
         sweep, args.no_cpu_baseline = [args.kchunk], True
@@ -344,59 +416,45 @@ def main():
     n_layers = len(M.meta)
     comm = dd.Comm() if world > 1 else None  # library-owned NCCL communicator (TP all-gather)
 
-    # ---- full decode-step graphs per k_chunk -------------------------------------------------
-    def step_launchers(kc):
-        if world == 1:
-            stacks = [dd.Stack(M.layers, M.ks(kc), M.xs(s), M.ys(), ws) for s in range(args.nx)]
-            return stacks, [st.launch for st in stacks], stacks[0].kernels
-        # TP: decdec_stack_create_tp -- every layer on this rank's shard + the library's in-place
-        # NCCL all-gather of y, captured as one native CUDA graph
-        full = [torch.empty(m[3] * world, dtype=torch.float16, device=dev) for m in M.meta]
-        stacks = [dd.TPStack(M.layers, M.ks(kc), M.xs(s), full, ws, comm) for s in range(args.nx)]
-        kern = stacks[0].kernels  # our kernels (+ one NCCL all-gather per layer, not counted)
-        return stacks, [st.launch for st in stacks], kern
-
-    results = {}
-    headline = None
-    clocks = None
-    for kc in sweep:
-        objs, launches, kernels = step_launchers(kc)
-        is_head = kc == args.kchunk
-        sampler = ClockSampler(local) if (is_head and rank == 0) else None
-        ms = time_graphs(torch, dist, launches, args.steps, max(args.warmup, 3), stream, world)
-        if sampler is not None:
-            clocks = sampler.stop()
-        results[kc] = {"ms_per_step": ms, "tokens_per_s": 1e3 / ms, "kernels_per_step": kernels}
-        if is_head:
-            headline = (ms, kernels)
-        del objs
+    # ---- full decode-step graphs per k_chunk (clocks sampled over all timed regions) ---------
+    sampler = ClockSampler(local) if rank == 0 else None
+    results = step_sweep(torch, dist, dd, M, ws, sweep, args.steps, args.warmup, stream, world, comm)
+    clocks = sampler.stop() if sampler is not None else None
+    headline = (results[args.kchunk]["ms_per_step"], results[args.kchunk]["kernels_per_step"])
 
     # ---- per-shape µs per layer (graph of the n_blocks instances of one shape) --------------
-    shape_names = []
-    for (_, name, _, _) in M.meta:
-        if name not in shape_names:
-            shape_names.append(name)
-    per_shape = {}
+    per_shape, per_unfused, w4 = {}, None, None
     if not (args.quick or args.sweep_only):  # per rank under TP: the rank's shards, no collective
-        for name in shape_names:
-            idx = [i for i, m in enumerate(M.meta) if m[1] == name]
-            d_in, d_out = M.meta[idx[0]][2], M.meta[idx[0]][3]
-            per_shape[name] = {"d_in": d_in, "d_out": d_out}
-            for kc in sweep:
-                lay = [M.layers[i] for i in idx]
-                xs = [M.xs(s) for s in range(args.nx)]
-                stacks = [dd.Stack(lay, M.ks(kc, idx), [xs[s][i] for i in idx], [M.ys()[i] for i in idx], ws)
-                          for s in range(args.nx)]
-                ms = time_graphs(torch, dist, [st.launch for st in stacks], max(8, args.steps // 4), 3, stream, world)  # max over ranks
-                us = 1e3 * ms / len(idx)
-                k = k_of(kc, d_in)
-                bh, bp = bytes_hbm(d_in, d_out, args.bits), bytes_pcie(k, d_out)
-                t_roof = max(bh / (hbm_peak * 1e3), bp / (pcie_peak * 1e3))  # µs
-                per_shape[name][str(kc)] = {"us": round(us, 3), "k": k, "hbm_GBps": round(bh / us / 1e3, 1),
-                                            "pcie_GBps": round(bp / us / 1e3, 2), "roofline_us": round(t_roof, 3),
-                                            "roofline_frac": round(t_roof / us, 3)}
-                for st in stacks:
-                    st.close()
+        per_shape = time_shapes(torch, dist, dd, M, ws, sweep, args.steps, stream, world, args.bits, hbm_peak,
+                                pcie_peak)
+        if not args.unfused and args.model == "llama3_8b" and not args.no_unfused_extra:
+            # the 7 unfused shapes: q = o and down = d shapes (timed above); k/v and gate/up on their
+            # own n_blocks instances
+            from synth import SHAPES
+            extra = [(n, *SHAPES[args.model][n]) for n in ("k", "gate")]
+            MX = Model(dd, torch, args.model, args.bits, rank, shard, args.nx, dev, shapes=extra, numa=numa)
+            wsx = dd.Workspace(k_of(max(sweep), MX.max_d_in), MX.max_d_out)
+            px = time_shapes(torch, dist, dd, MX, wsx, sweep, args.steps, stream, world, args.bits, hbm_peak,
+                             pcie_peak)
+            per_unfused = {"q": per_shape["o"], "k": px["k"], "v": px["k"], "o": per_shape["o"],
+                           "gate": px["gate"], "up": px["gate"], "down": per_shape["d"],
+                           "_note": "same-shape pairs timed once: q = o (4096x4096), v = k (4096x1024), "
+                                    "up = gate (4096x14336), down = d (14336x4096)"}
+            del MX, wsx
+        if not args.no_w4 and args.bits == 3 and world == 1:
+            # config 3: the same stack with 4-bit base weights (the residual store is shared)
+            M4 = Model(dd, torch, args.model, 4, rank, shard, args.nx, dev, fused=not args.unfused, hosts=M.hosts,
+                       numa=numa)
+            w4_sweep = sorted({0, 4, 8, args.kchunk})
+            r4 = step_sweep(torch, dist, dd, M4, ws, w4_sweep, args.steps, args.warmup, stream, world)
+            w4 = {"config": "BASELINE configs[2]: Llama-3-8B 4-bit (W4K, g128 fp16 s + u8 z) + r4 residual",
+                  "sweep": {str(k): {"tokens_per_s": round(v["tokens_per_s"], 2), "ms_per_step": round(v["ms_per_step"], 4),
+                                     "slowdown_vs_k0": round(v["ms_per_step"] / r4[0]["ms_per_step"], 4)}
+                            for k, v in r4.items()},
+                  "knee": knee(r4, 4, hbm_peak, pcie_peak),
+                  "per_layer_us": time_shapes(torch, dist, dd, M4, ws, [0, args.kchunk], args.steps, stream, world, 4,
+                                              hbm_peak, pcie_peak)}
+            del M4
 
     # ---- e2e through the public API: H2D inputs + step + D2H outputs ------------------------
     e2e = None
@@ -505,7 +563,10 @@ def main():
                                "slowdown_vs_k0": round(v["ms_per_step"] / results[0]["ms_per_step"], 4)
                                if 0 in results else None}
                       for k, v in results.items()},
+            "knee": knee(results, args.bits, hbm_peak, pcie_peak),
             "per_layer_us": per_shape,
+            "per_layer_us_unfused": per_unfused,
+            "w4": w4,
             "step_bytes": {"hbm": step_hbm, "pcie": step_pcie},
             "build_s": round(t_build, 1),
         }

@@ -122,7 +122,9 @@ decdec_status decdec_gemv(const decdec_layer* L, const uint16_t* x, uint16_t* y,
                           size_t ws_bytes, decdec_stream_t stream);
 
 /* Step (1) alone: exact Top-k (S:117-131 exact_topk).  idx: device int32 [n_sel],
- * xs: device fp16 [n_sel]; n_sel = k (chunk = 0) or sum_c min(k, len_c) (chunk > 0). */
+ * xs: device fp16 [n_sel]; n_sel = k (chunk = 0) or sum_c min(k, len_c) (chunk > 0).
+ * x: device fp16 [d_in], 16-B aligned, d_in % 8 == 0, d_in <= 32768 (else DECDEC_EINVAL /
+ * DECDEC_EALIGN; idx 4-B and xs 2-B aligned). */
 decdec_status decdec_select(const uint16_t* x, int32_t d_in, int32_t k, int32_t chunk,
                             int32_t* idx, uint16_t* xs, decdec_stream_t stream);
 
@@ -200,19 +202,35 @@ decdec_status decdec_pack_residual(const int8_t* c, int32_t d_in, int32_t d_out,
 decdec_status decdec_host_alloc(size_t bytes, int32_t numa_node, int32_t write_combined, void** p);
 void decdec_host_free(void* p);
 
+/* NUMA node of a CUDA device's PCIe attachment (/sys/bus/pci/devices/<bdf>/numa_node), for
+ * binding each rank's residual slice to the socket in front of its own PCIe link (SURVEY.md
+ * §8(e)); -1 when unknown (no NUMA, bad device).  Host-only, no GPU work. */
+int32_t decdec_device_numa_node(int32_t device);
+
 /* ------------------------------------------------------------------ debug / introspection */
 /* Decode the packed weights with the GEMV kernel's own in-register decode path and write
  * the integer codes to q_out (device u8 [d_out][d_in]).  For bit-exact layout tests. */
 decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out,
                                           decdec_stream_t stream);
 
-/* Debug timelines: while buf != NULL every launch records %globaltimer (ns) events into buf
- * (u64: [0..1] unused, then per CTA 9 events: start, first bulk copy issued, x loaded, first
- * stage landed, GEMV done, selector start / selection staged, selection published, gather
- * done; selector CTAs come first).  bytes >= (2 + 1024*9)*8.  Stacks created while tracing give
- * layer i the region starting at u64 2 + i*160*20 (bytes >= (2 + n_layers*3200)*8).  Not
- * thread-safe; NULL disables. */
+/* Debug timelines: while buf != NULL every launch records %globaltimer (ns) / SM-cycle events
+ * into buf (u64: [0..1] unused, then per CTA 20 events, see csrc/linear.cuh kTraceEvents:
+ * 0 start, 2 x loaded, 3 first stage landed, 4 GEMV done, 5 selector start, 6 selection
+ * published, 7 gather done, 9 combine done, 10 last warp exits, 12 partials published, 14-19
+ * selector phases in SM cycles; DEC CTAs come first).  Single calls: bytes >= (2 + 1024*20)*8.
+ * Stacks created while tracing give layer i the region starting at u64 2 + i*160*20; their
+ * creation fails with DECDEC_ESPACE unless bytes >= (2 + n_layers*3200)*8.  Not thread-safe;
+ * NULL disables. */
 decdec_status decdec_debug_trace(void* buf, size_t bytes);
+
+/* Debug (tests): while idx != NULL, every DEC CTA c < max_ctas of each compensated launch
+ * (the CTAs that select, gather and combine; each computes the selection itself)
+ * writes its own selected indices / x[S] in its placement order (a permutation of the
+ * ascending selection) to idx[c*cap ...] / xs[c*cap ...] (device int32 / fp16, at most cap
+ * entries each).  Lets tests check EVERY DEC CTA's selection bit-exact, not only the `sel`
+ * output of CTA 0.  idx = NULL disables.  DECDEC_EINVAL if cap or max_ctas <= 0.  Not
+ * thread-safe; process-wide. */
+decdec_status decdec_debug_selections(int32_t* idx, uint16_t* xs, int32_t cap, int32_t max_ctas);
 
 /* Launch plan chosen for a layer (tile rows, consumer warps, stages, grid) as text. */
 decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, size_t buf_bytes);

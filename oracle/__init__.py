@@ -32,4 +32,5 @@ from .decdec_ref import (  # noqa: F401
     unpack_w3k_ref,
     unpack_rq_ref,
     tolerance_ok,
+    rel_err_unfloored,
 )

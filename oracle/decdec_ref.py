@@ -23,6 +23,9 @@ Functions and their pins (tests/test_oracle_*.py):
                         over disjoint selections, empty selection.
   O6 pack_*_ref         pinned: hand-derived golden words (tests/golden/pack_words.txt)
                         and unpack(pack(q)) == q round trips.
+  L9 tolerance_ok       pinned: hand-constructed accept/reject cases at 0.99e-3 / 1.01e-3 |y*|,
+                        each floor engaging where it dominates, sign flips rejected
+                        (tests/test_oracle_tolerance.py); rel_err_unfloored likewise.
 
 Parity unpinned: none of the functions above; large-shape GEMV values have no
 paper-printed worked example (P:147-152 is figure-only), so they rest on the
@@ -185,7 +188,7 @@ def topk_ref(x16, k: int, chunk: int = 0):
 
 
 # ----------------------------------------------------------------------------- O5
-def decdec_linear_ref(q, s, z, x16, k: int, chunk: int = 0, rc=None, rS=None, r16=None):
+def decdec_linear_ref(q, s, z, x16, k: int, chunk: int = 0, rc=None, rS=None, r16=None, W_hat=None):
     """O5: y = W_hat x + sum_{i in S} x_i R_hat[i, :] in float64 (P:204-207 steps 1-4).
 
     q uint8 [d_in, d_out], s fp16 [G, d_out], z uint8 [G, d_out]: base weights (O1 format).
@@ -194,8 +197,11 @@ def decdec_linear_ref(q, s, z, x16, k: int, chunk: int = 0, rc=None, rS=None, r1
     parity samples outputs.
     Returns dict: idx, xs (selection), ob, odec, y64, y16 (fp16_rne of y64), A
     (A_j = sum_i |W_hat_ij x_i| + sum_{i in S} |R_hat_ij x_i|, the L9 scale).
+    W_hat: optional precomputed dequantize_base(q, s, z) (same values; lets a test reuse
+    it across calls on one layer instead of rebuilding it per call).
     """
-    W_hat = dequantize_base(q, s, z)
+    if W_hat is None:
+        W_hat = dequantize_base(q, s, z)
     x = np.asarray(x16, dtype=np.float16).astype(np.float64)
     ob = x @ W_hat                                   # step: o_b = W_hat x
     A = np.abs(x) @ np.abs(W_hat)
@@ -225,12 +231,30 @@ def decdec_linear_ref_cols(q, s, z, x16, k, cols, chunk=0, rc=None, rS=None, r16
 
 
 def tolerance_ok(y16, y64, A):
-    """Ledger L9: |y16 - y*| <= 1e-3 * max(|y*|, 2^-12 A_j, 2^-14) (BJ 'max relative error 1e-3')."""
+    """Ledger L9: |y16 - y*| <= 1e-3 * max(|y*|, 2^-12 A_j, 2^-14) (BJ 'max relative error 1e-3').
+
+    Pinned by hand-constructed cases (tests/test_oracle_tolerance.py): an error of 1.01e-3 |y*|
+    is rejected and 0.99e-3 |y*| accepted; each floor (2^-12 A_j, 2^-14) engages exactly where
+    it exceeds |y*|; a sign flip is rejected.
+    """
     y = np.asarray(y16, dtype=np.float16).astype(np.float64)
     y64 = np.asarray(y64, dtype=np.float64)
     bound = 1e-3 * np.maximum(np.maximum(np.abs(y64), 2.0 ** -12 * np.asarray(A)), 2.0 ** -14)
     err = np.abs(y - y64)
     return err <= bound, err, bound
+
+
+def rel_err_unfloored(y16, y64):
+    """Ledger L9 report: max |y16 - y*| / |y*| over the outputs with |y*| >= 1e-2 * rms(y*)
+    (the unfloored relative error; outputs near zero are excluded, not floored).
+    Returns (max relative error, number of outputs it was taken over)."""
+    y = np.asarray(y16, dtype=np.float16).astype(np.float64)
+    y64 = np.asarray(y64, dtype=np.float64)
+    rms = np.sqrt(np.mean(y64 ** 2)) if y64.size else 0.0
+    m = np.abs(y64) >= 1e-2 * rms
+    if not m.any():
+        return 0.0, 0
+    return float(np.max(np.abs(y[m] - y64[m]) / np.abs(y64[m]))), int(m.sum())
 
 
 # ----------------------------------------------------------------------------- O6 packing

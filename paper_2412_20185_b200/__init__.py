@@ -14,6 +14,9 @@ from ._lib import (  # noqa: F401
     decdec_comm_init,
     decdec_comm_nranks,
     decdec_comm_rank,
+    decdec_debug_selections,
+    decdec_device_numa_node,
+    numa_node_of_device,
     decdec_debug_trace,
     decdec_debug_unpack_weights,
     decdec_gemv,

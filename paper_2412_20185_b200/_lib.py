@@ -51,10 +51,12 @@ def _load():
         "decdec_pack_residual": (I32, [VP, I32, I32, VP, SZ]),
         "decdec_host_alloc": (I32, [SZ, I32, I32, P(VP)]),
         "decdec_host_free": (None, [VP]),
+        "decdec_device_numa_node": (I32, [I32]),
         "decdec_debug_unpack_weights": (I32, [Lp, VP, VP]),
         "decdec_plan_string": (I32, [Lp, I32, ctypes.c_char_p, SZ]),
         "decdec_launches_per_call": (I32, [I32]),
         "decdec_debug_trace": (I32, [VP, SZ]),
+        "decdec_debug_selections": (I32, [VP, VP, I32, I32]),
         "decdec_stack_create": (I32, [Lp, I32, P(I32), I32, P(VP), P(VP), VP, SZ, VP, P(VP)]),
         "decdec_stack_launch": (I32, [VP, VP]),
         "decdec_stack_kernels": (I32, [VP]),
@@ -82,9 +84,9 @@ _lib = _load()
 EXPORTED = [
     "decdec_workspace_bytes", "decdec_workspace_init", "decdec_linear", "decdec_gemv", "decdec_select",
     "decdec_num_selected", "decdec_pack_weights", "decdec_pack_residual", "decdec_host_alloc",
-    "decdec_host_free", "decdec_debug_unpack_weights", "decdec_plan_string", "decdec_launches_per_call",
+    "decdec_host_free", "decdec_device_numa_node", "decdec_debug_unpack_weights", "decdec_plan_string", "decdec_launches_per_call",
     "decdec_status_string", "decdec_version", "decdec_stack_create", "decdec_stack_launch",
-    "decdec_stack_kernels", "decdec_stack_destroy", "decdec_debug_trace",
+    "decdec_stack_kernels", "decdec_stack_destroy", "decdec_debug_trace", "decdec_debug_selections",
     "decdec_set_dec_ctas", "decdec_nccl_version", "decdec_nccl_unique_id", "decdec_comm_init", "decdec_comm_destroy",
     "decdec_comm_rank", "decdec_comm_nranks", "decdec_linear_tp", "decdec_stack_create_tp",
 ]
@@ -137,6 +139,15 @@ def decdec_host_alloc(nbytes: int, numa_node: int = -1, write_combined: int = 0)
     p = ctypes.c_void_p()
     _check(_lib.decdec_host_alloc(nbytes, numa_node, write_combined, ctypes.byref(p)), "decdec_host_alloc")
     return int(p.value)
+
+
+def decdec_device_numa_node(device: int) -> int:
+    return int(_lib.decdec_device_numa_node(device))
+
+
+def numa_node_of_device(device: int) -> int:
+    """NUMA node in front of the GPU's PCIe link (-1 if unknown): where its residual slice goes."""
+    return decdec_device_numa_node(device)
 
 
 def decdec_host_free(p):
@@ -198,6 +209,11 @@ def decdec_debug_trace(buf, nbytes):
 
 
 # ------------------------------------------------------------------ tensor parallelism
+def decdec_debug_selections(idx, xs, cap: int, max_ctas: int):
+    """Debug: every DEC CTA c < max_ctas writes its own selection to idx/xs[c*cap ...] (0 = off)."""
+    _check(_lib.decdec_debug_selections(_vp(idx), _vp(xs), cap, max_ctas), "decdec_debug_selections")
+
+
 def decdec_nccl_version() -> int:
     return int(_lib.decdec_nccl_version())
 

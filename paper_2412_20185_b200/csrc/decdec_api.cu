@@ -7,6 +7,7 @@
 #include <mutex>
 
 #include "decdec.h"
+#include "gemv.cuh"
 #include "linear.cuh"
 #include "select.cuh"
 #include "tp_internal.h"
@@ -31,6 +32,10 @@ int device_sms() {
 }
 
 unsigned long long* g_trace = nullptr;  // debug timelines (decdec_debug_trace)
+size_t g_trace_bytes = 0;
+int* g_dbg_idx = nullptr;  // debug: every DEC CTA's own selection (decdec_debug_selections)
+uint16_t* g_dbg_xs = nullptr;
+int g_dbg_cap = 0, g_dbg_ctas = 0;
 constexpr size_t kTraceStride = 160 * 20;  // u64 per layer in stack traces (<= 160 CTAs)
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -86,7 +91,13 @@ bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, double 
   const uint32_t off_sel = (uint32_t)align_up(sel_bytes, 16);
   const uint32_t off_part = (uint32_t)align_up((size_t)off_sel + (size_t)k_sel * 6, 16);
   const size_t row_b = max_rpi == kGatherRows16 ? 16 : 4;  // bytes per lane per staged row
-  for (int nd = dec_ctas(warps, r); nd <= 96; nd *= 2) {
+  // A DEC CTA without a segment would only select and exit while holding an SM the GEMV
+  // needs; and at least half of the SMs stay GEMV CTAs (no plan where DEC CTAs fill the GPU).
+  const int nd_max = p->n_seg < device_sms() / 2 ? p->n_seg : device_sms() / 2;
+  int nd_first = dec_ctas(warps, r);
+  if (nd_first > nd_max) nd_first = nd_max;
+  if (nd_first < 1) nd_first = 1;
+  for (int nd = nd_first; nd <= nd_max; nd = (nd == nd_max ? nd_max + 1 : (2 * nd < nd_max ? 2 * nd : nd_max))) {
     const int ns = (p->n_seg + nd - 1) / nd;
     const int gws_target = (warps + ns - 1) / ns;
     // staging rows per buffer: as many as fit (<= max_rpi); fewer rows -> more, smaller items
@@ -182,6 +193,7 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
       if (k_sel > 0 && !plan_dec(d_out, k_sel, sel_len, 1 + nc, r_bits == 16 ? kGatherRows16 : kGatherRows4, r_ratio, &p))
         continue;
       const int max_grid = sms - p.n_dec;
+      if (max_grid <= 0) continue;
       p.grid = p.n_tiles < max_grid ? p.n_tiles : max_grid;
       if (p.smem > kSmemBudget + 16 * 1024) continue;
       const double waves = (double)((p.n_tiles + max_grid - 1) / max_grid);
@@ -197,6 +209,98 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
   }
   if (!have) return DECDEC_EUNSUPPORTED;
   *pl = best;
+  return DECDEC_OK;
+}
+
+// ---------------------------------------------------------------- k_gemv plan (k = 0)
+// Two CTAs per SM: <= kGemvSmemBudget dynamic smem each.  Team shape (T warps, M rows per pass)
+// maximises the issuing lanes that own a (row, group): efficiency M*G / (32 * ceil(M*G/32)),
+// ties -> smaller T.  RPS (passes per stage): the largest with >= 3 ring stages, else >= 2.
+constexpr size_t kGemvSmemBudget = 110 * 1024;     // NC = 8: two CTAs per SM
+constexpr size_t kGemvSmemBudget16 = 200 * 1024;   // NC = 16: one CTA per SM
+
+// DECDEC_GEMV_NC = 8 | 16 (A/B knob; default below)
+int gemv_nc() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DECDEC_GEMV_NC");
+    env = e ? atoi(e) : 16;
+    if (env != 8) env = 16;
+  }
+  return env;
+}
+struct GemvPlan {
+  GemvParams gp;
+  size_t smem;
+  int grid;
+};
+
+decdec_status make_gemv_plan(int d_in, int d_out, int bits, int n_cta_max, GemvPlan* out) {
+  const int G = d_in / DECDEC_GROUP;
+  GemvParams g{};
+  g.d_in = d_in;
+  g.d_out = d_out;
+  g.G = G;
+  g.row_bytes = d_in * bits / 8;
+  const int NC = gemv_nc();
+  const size_t budget = NC == 8 ? kGemvSmemBudget : kGemvSmemBudget16;
+  g.NC = NC;
+  int bestT = 0, bestM = 0;
+  double best_eff = -1.0;
+  for (int T = 1; T <= NC; T *= 2) {
+    const int M = 32 * T / G;
+    if (M < 1) continue;
+    const int lanes = M * G, warps = (lanes + 31) / 32;
+    const double eff = (double)lanes / (32.0 * warps);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      bestT = T;
+      bestM = M;
+    }
+  }
+  if (!bestT) return DECDEC_EUNSUPPORTED;  // G > 256: d_in > 32768
+  g.T = bestT;
+  g.M = bestM;
+  g.team_red = !(bestT == 1 && 32 % G == 0);
+  int Q = 1;
+  while ((Q * G) % 16) ++Q;  // rows*G bytes of zeros (and 2x of scales) stay 16-B multiples
+  g.Q = Q;
+  const int nteam = NC / bestT;
+  const size_t xb = align_up((size_t)d_in * 2, 16);
+  bool ok = false;
+  for (int need = 3; need >= 2 && !ok; --need) {
+    for (int rps = kGemvMaxRPS; rps >= 1; rps /= 2) {
+      const int TRS = nteam * bestM * rps;
+      if (TRS % Q) continue;
+      const uint32_t off_s = (uint32_t)align_up((size_t)TRS * g.row_bytes, 16);
+      const uint32_t off_z = off_s + (uint32_t)align_up((size_t)TRS * G * 2, 16);
+      const uint32_t sb = (uint32_t)align_up((size_t)off_z + (size_t)TRS * G, 128);
+      const size_t red = g.team_red ? align_up((size_t)2 * TRS * G * 4, 16) : 0;
+      const size_t fixed = xb + red + 16 * 8;
+      if (fixed + (size_t)need * sb > budget) continue;
+      int stages = (int)((budget - fixed) / sb);
+      if (stages > 8) stages = 8;
+      g.RPS = rps;
+      g.TRS = TRS;
+      g.stages = stages;
+      g.stage_bytes = sb;
+      g.off_s = off_s;
+      g.off_z = off_z;
+      g.off_x = (uint32_t)((size_t)stages * sb);
+      g.off_red = (uint32_t)align_up((size_t)g.off_x + xb, 16);
+      g.off_bar = (uint32_t)align_up((size_t)g.off_red + red, 16);
+      out->smem = (size_t)g.off_bar + 2 * (size_t)stages * 8;
+      ok = true;
+      break;
+    }
+  }
+  if (!ok) return DECDEC_EUNSUPPORTED;
+  const int units = d_out / Q;
+  g.n_cta = units < n_cta_max ? units : n_cta_max;
+  g.cta0 = 0;
+  g.x_pf = 1;
+  out->grid = g.n_cta;
+  out->gp = g;
   return DECDEC_OK;
 }
 
@@ -224,9 +328,12 @@ decdec_status set_smem_attr(K kern, size_t bytes) {
   return cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-std::once_flag g_attr_once;
-decdec_status g_attr_status = DECDEC_OK;
-void init_attrs() {
+// Kernel attributes (max dynamic smem) are per device: initialise once per device.
+constexpr int kMaxDevices = 64;
+std::mutex g_attr_mu;
+int g_attr_done[kMaxDevices] = {0};
+decdec_status g_attr_status[kMaxDevices];
+decdec_status init_attrs() {
   decdec_status s = DECDEC_OK;
   const size_t lin = 226 * 1024;  // + static smem <= 227 KB
   if (s == DECDEC_OK) s = set_smem_attr(k_select, 80 * 1024);
@@ -234,11 +341,25 @@ void init_attrs() {
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 16>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 16>, lin);
-  g_attr_status = s;
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv<3>, kGemvSmemBudget + 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv<4>, kGemvSmemBudget + 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<3>, kGemvSmemBudget16 + 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<4>, kGemvSmemBudget16 + 1024);
+  // two k_gemv CTAs (this layer's and the next one's) must fit an SM's shared memory: ask for
+  // the maximum shared-memory carveout so the SM is not configured for fewer
+  if (s == DECDEC_OK) s = cuda_status(cudaFuncSetAttribute(k_gemv<3>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  if (s == DECDEC_OK) s = cuda_status(cudaFuncSetAttribute(k_gemv<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  return s;
 }
 decdec_status ensure_attrs() {
-  std::call_once(g_attr_once, init_attrs);
-  return g_attr_status;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return DECDEC_ECUDA;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (!g_attr_done[dev]) {
+    g_attr_status[dev] = init_attrs();
+    g_attr_done[dev] = 1;
+  }
+  return g_attr_status[dev];
 }
 
 bool is_device_ptr(const void* p) {
@@ -314,6 +435,42 @@ decdec_status launch_linear(const LinearParams& p, const Plan& pl, int bits, int
   return rbits == 16 ? launch_linear_t<4, 16>(p, pl, pdl, st) : launch_linear_t<4, 4>(p, pl, pdl, st);
 }
 
+decdec_status launch_gemv(const GemvPlan& pl, int bits, bool pdl, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(32 * (1 + pl.gp.NC));
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (pl.gp.NC == 8)
+    return cuda_status(bits == 3 ? cudaLaunchKernelEx(&cfg, k_gemv<3>, pl.gp) : cudaLaunchKernelEx(&cfg, k_gemv<4>, pl.gp));
+  return cuda_status(bits == 3 ? cudaLaunchKernelEx(&cfg, k_gemv16<3>, pl.gp) : cudaLaunchKernelEx(&cfg, k_gemv16<4>, pl.gp));
+}
+
+// DECDEC_L2PF_NEXT=0 disables the stack executor's cross-layer L2 prefetch (A/B only)
+bool l2_next_prefetch() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DECDEC_L2PF_NEXT");
+    env = e ? (atoi(e) > 0) : 1;
+  }
+  return env == 1;
+}
+
+// DECDEC_OLD_GEMV=1: k = 0 calls use the fused kernel's GEMV CTAs (round-1 path; A/B only)
+bool use_gemv_kernel() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DECDEC_OLD_GEMV");
+    env = (e && atoi(e) > 0) ? 0 : 1;
+  }
+  return env == 1;
+}
+
 LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, const Plan& pl) {
   LinearParams p{};
   p.w = static_cast<const uint8_t*>(L->w_packed);
@@ -342,6 +499,10 @@ LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, 
   p.off_stage = pl.off_stage;
   p.off_x = pl.off_x;
   p.trace = g_trace ? g_trace + 2 : nullptr;
+  p.dbg_idx = g_dbg_idx;
+  p.dbg_xs = g_dbg_xs;
+  p.dbg_cap = g_dbg_cap;
+  p.dbg_ctas = g_dbg_ctas;
   static int env_prefetch = -1;
   if (env_prefetch < 0) {
     const char* e = getenv("DECDEC_PREFETCH");
@@ -386,8 +547,10 @@ int32_t decdec_num_selected(int32_t d_in, int32_t k, int32_t chunk) { return n_s
 decdec_status decdec_select(const uint16_t* x, int32_t d_in, int32_t k, int32_t chunk, int32_t* idx, uint16_t* xs,
                             decdec_stream_t stream) {
   if (!x || !idx || !xs) return DECDEC_EINVAL;
-  if (d_in <= 0 || d_in > 32768) return DECDEC_EINVAL;
+  if (d_in <= 0 || d_in > 32768 || d_in % 8) return DECDEC_EINVAL;  // the selector reads x as 16-B chunks
   if (n_selected(d_in, k, chunk) < 0) return DECDEC_EINVAL;
+  if (!aligned16(x) || (reinterpret_cast<uintptr_t>(idx) & 3u) || (reinterpret_cast<uintptr_t>(xs) & 1u))
+    return DECDEC_EALIGN;
   decdec_status s = ensure_attrs();
   if (s != DECDEC_OK) return s;
   if (k == 0) return DECDEC_OK;
@@ -403,6 +566,17 @@ decdec_status decdec_gemv(const decdec_layer* L, const uint16_t* x, uint16_t* y,
   if (!x || !y) return DECDEC_EINVAL;
   if (!aligned16(x) || !aligned16(y)) return DECDEC_EALIGN;
   if ((s = ensure_attrs()) != DECDEC_OK) return s;
+  if (use_gemv_kernel()) {
+    GemvPlan gpl;
+    if ((s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &gpl)) != DECDEC_OK) return s;
+    gpl.gp.w = static_cast<const uint8_t*>(L->w_packed);
+    gpl.gp.ws = L->w_scales;
+    gpl.gp.wz = L->w_zeros;
+    gpl.gp.x = x;
+    gpl.gp.y = y;
+    gpl.gp.trace = g_trace ? g_trace + 2 : nullptr;
+    return launch_gemv(gpl, L->w_bits, false, (cudaStream_t)stream);
+  }
   Plan pl;
   if ((s = make_plan(L->d_in, L->d_out, L->w_bits, 0, &pl)) != DECDEC_OK) return s;
   LinearParams p = base_params(L, x, y, pl);
@@ -418,6 +592,8 @@ namespace {
 struct Prepared {
   LinearParams p;
   Plan pl;
+  bool gemv;  // k = 0: the two-CTAs-per-SM base GEMV kernel (gemv.cuh)
+  GemvPlan gpl;
   int k, chunk, bits, rbits;
   const uint16_t* x;
   int32_t* sel;
@@ -433,6 +609,26 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
   if (k_sel < 0) return DECDEC_EINVAL;
   if ((s = ensure_attrs()) != DECDEC_OK) return s;
   Prepared P{};
+  if (k_sel == 0 && use_gemv_kernel()) {
+    if ((s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &P.gpl)) != DECDEC_OK) return s;
+    GemvParams& g = P.gpl.gp;
+    g.w = static_cast<const uint8_t*>(L->w_packed);
+    g.ws = L->w_scales;
+    g.wz = L->w_zeros;
+    g.x = x;
+    g.y = y;
+    g.ob = nullptr;
+    g.trace = g_trace ? g_trace + 2 : nullptr;
+    P.gemv = true;
+    P.k = k;
+    P.chunk = chunk;
+    P.bits = L->w_bits;
+    P.rbits = L->r_bits;
+    P.x = x;
+    P.sel = sel;
+    *out = P;
+    return DECDEC_OK;
+  }
   const int sel_len = chunk ? (chunk < L->d_in ? chunk : L->d_in) : L->d_in;
   if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &P.pl, sel_len, L->r_bits)) != DECDEC_OK)
     return s;
@@ -469,6 +665,7 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
 }
 
 decdec_status enqueue_linear(const Prepared& P, cudaStream_t st, bool chained = false) {
+  if (P.gemv) return launch_gemv(P.gpl, P.bits, chained, st);
   Plan pl = P.pl;
   pl.grid += P.pl.n_dec;  // DEC CTAs first
   return launch_linear(P.p, pl, P.bits, P.p.k_sel ? P.rbits : 4, chained, st);
@@ -503,6 +700,7 @@ decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const i
                            decdec_comm* comm, decdec_stack** out) {
   if (!layers || n_layers <= 0 || !k || !x || !y || !out) return DECDEC_EINVAL;
   *out = nullptr;
+  if (g_trace && g_trace_bytes < (2 + (size_t)n_layers * kTraceStride) * 8) return DECDEC_ESPACE;
   const int rank = comm ? tp_rank(comm) : 0;
   const bool gather = comm && decdec_comm_nranks(comm) > 1;
   Prepared* P = new Prepared[n_layers];
@@ -512,12 +710,29 @@ decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const i
     uint16_t* yi = y[i] ? y[i] + (size_t)rank * layers[i].d_out : nullptr;
     s = prepare_linear(&layers[i], x[i], k[i], chunk, yi, nullptr, ws, ws_bytes, &P[i]);
     // debug timelines: one trace region per layer (decdec_debug_trace buffer must hold them)
-    if (g_trace) P[i].p.trace = g_trace + 2 + (size_t)i * kTraceStride;
+    if (g_trace) {
+      P[i].p.trace = g_trace + 2 + (size_t)i * kTraceStride;
+      P[i].gpl.gp.trace = g_trace + 2 + (size_t)i * kTraceStride;
+    }
     n_kernels += 1;
   }
   if (s != DECDEC_OK) {
     delete[] P;
     return s;
+  }
+  if (l2_next_prefetch() && n_layers > 1) {
+    for (int i = 0; i < n_layers; ++i) {
+      if (!P[i].gemv) continue;
+      const decdec_layer& Ln = layers[(i + 1) % n_layers];
+      const int Gn = Ln.d_in / DECDEC_GROUP;
+      GemvParams& g = P[i].gpl.gp;
+      g.pf_ptr[0] = static_cast<const uint8_t*>(Ln.w_packed);
+      g.pf_bytes[0] = (uint32_t)((size_t)Ln.d_out * Ln.d_in * Ln.w_bits / 8);
+      g.pf_ptr[1] = reinterpret_cast<const uint8_t*>(Ln.w_scales);
+      g.pf_bytes[1] = (uint32_t)((size_t)Ln.d_out * Gn * 2);
+      g.pf_ptr[2] = Ln.w_zeros;
+      g.pf_bytes[2] = (uint32_t)((size_t)Ln.d_out * Gn);
+    }
   }
   cudaStream_t st = nullptr;
   cudaError_t e0 = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
@@ -609,6 +824,17 @@ decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out,
 decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, size_t buf_bytes) {
   if (!L || !buf) return DECDEC_EINVAL;
   const int k_sel = k;  // caller passes the selected count
+  if (k_sel == 0 && use_gemv_kernel()) {
+    GemvPlan g;
+    decdec_status s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &g);
+    if (s != DECDEC_OK) return s;
+    snprintf(buf, buf_bytes,
+             "{\"kernel\": \"k_gemv\", \"G\": %d, \"T\": %d, \"M\": %d, \"team_red\": %d, \"RPS\": %d, \"TRS\": %d, "
+             "\"Q\": %d, \"NC\": %d, \"stages\": %d, \"stage_bytes\": %u, \"grid\": %d, \"threads\": %d, \"smem\": %zu}",
+             g.gp.G, g.gp.T, g.gp.M, g.gp.team_red, g.gp.RPS, g.gp.TRS, g.gp.Q, g.gp.NC, g.gp.stages, g.gp.stage_bytes,
+             g.grid, 32 * (1 + g.gp.NC), g.smem);
+    return DECDEC_OK;
+  }
   Plan pl;
   decdec_status s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &pl);
   if (s != DECDEC_OK) return s;
@@ -634,6 +860,22 @@ int32_t decdec_launches_per_call(int32_t k) {
 decdec_status decdec_debug_trace(void* buf, size_t bytes) {
   if (buf && bytes < (size_t)(2 + 1024 * kTraceEvents) * 8) return DECDEC_ESPACE;
   g_trace = static_cast<unsigned long long*>(buf);
+  g_trace_bytes = buf ? bytes : 0;
+  return DECDEC_OK;
+}
+
+decdec_status decdec_debug_selections(int32_t* idx, uint16_t* xs, int32_t cap, int32_t max_ctas) {
+  if (!idx || !xs) {
+    g_dbg_idx = nullptr;
+    g_dbg_xs = nullptr;
+    g_dbg_cap = g_dbg_ctas = 0;
+    return DECDEC_OK;
+  }
+  if (cap <= 0 || max_ctas <= 0) return DECDEC_EINVAL;
+  g_dbg_idx = idx;
+  g_dbg_xs = xs;
+  g_dbg_cap = cap;
+  g_dbg_ctas = max_ctas;
   return DECDEC_OK;
 }
 

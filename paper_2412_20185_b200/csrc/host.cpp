@@ -170,6 +170,24 @@ const char* decdec_status_string(decdec_status s) {
   return "unknown status";
 }
 
-const char* decdec_version(void) { return "decdec-b200 0.1 (sm_100a)"; }
+const char* decdec_version(void) { return "decdec-b200 0.2 (sm_100a)"; }
+
+int32_t decdec_device_numa_node(int32_t device) {
+  char bdf[32] = {0};
+  if (cudaDeviceGetPCIBusId(bdf, (int)sizeof bdf, device) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  for (char* c = bdf; *c; ++c)  // sysfs uses lower-case hex ("0000:e5:00.0")
+    if (*c >= 'A' && *c <= 'F') *c = (char)(*c - 'A' + 'a');
+  char path[96];
+  snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bdf);
+  FILE* f = fopen(path, "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  return node >= 0 ? node : -1;
+}
 
 }  // extern "C"

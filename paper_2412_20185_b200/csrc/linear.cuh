@@ -90,6 +90,11 @@ struct LinearParams {
   int l2pf;      // further tiles per CTA prefetched into L2 only before griddepcontrol.wait
   int x_pf;      // prefetch x into L2 before griddepcontrol.wait
   int* sel_out;
+  // debug (decdec_debug_selections): DEC CTA c < dbg_ctas writes its own S / x[S] (in its
+  // placement order) to dbg_idx[c * dbg_cap ...] / dbg_xs[...]; null = off
+  int* dbg_idx;
+  uint16_t* dbg_xs;
+  int dbg_cap, dbg_ctas;
 };
 
 // A DEC CTA (steps 1-4 of P:207).  DEC CTA c owns the output segments c, c + n_dec, ...:
@@ -342,6 +347,15 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     }
   }
   if (threadIdx.x == 0) DECDEC_TRACE(p, 9);
+  if (p.dbg_idx && (int)blockIdx.x < p.dbg_ctas) {  // every DEC CTA's own selection, for tests
+    if (split && nD < p.k_sel) select_wait_rest(SS);
+    int* di = p.dbg_idx + (size_t)blockIdx.x * p.dbg_cap;
+    uint16_t* dx = p.dbg_xs + (size_t)blockIdx.x * p.dbg_cap;
+    for (int i = threadIdx.x; i < p.k_sel && i < p.dbg_cap; i += blockDim.x) {
+      di[i] = sidx[i];
+      dx[i] = sxs[i];
+    }
+  }
 }
 
 template <int BITS, int RBITS>

@@ -121,6 +121,9 @@ def gen_perf_layer_device(d_in: int, d_out: int, bits: int, seed: int, device="c
     z = torch.randint(zlo, zlo + 2, (d_out * G,), dtype=torch.uint8, device=device, generator=g)
     ln = torch.exp(torch.randn(d_out * G, device=device, generator=g) * 0.25)
     s = (0.02 * 12 ** 0.5 / (1 << bits) * ln).to(torch.float16)
-    r = torch.randint(0, 256, (d_in * d_out // 2,), dtype=torch.uint8, device=device, generator=g)
+    nb_r = d_in * d_out // 2
+    lo = torch.randint(1, 16, (nb_r,), dtype=torch.uint8, device=device, generator=g)
+    hi = torch.randint(1, 16, (nb_r,), dtype=torch.uint8, device=device, generator=g)
+    r = lo | (hi << 4)
     rS = (s.float().view(d_out, G).median(dim=1).values / 14.0).to(torch.float16)
     return dict(w=w, s=s, z=z, r=r, rS=rS)
