@@ -379,6 +379,7 @@ def main():
                          "q = o and down = d shapes)")
     ap.add_argument("--no-w4", action="store_true", help="skip the 4-bit (config 3) sub-object")
     ap.add_argument("--no-unfused-extra", action="store_true", help="skip timing the k/v and gate/up shapes")
+    ap.add_argument("--no-lut", action="store_true", help="skip the non-uniform (LUT) base sub-object (NEXT-3)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -455,6 +456,36 @@ def main():
                   "per_layer_us": time_shapes(torch, dist, dd, M4, ws, [0, args.kchunk], args.steps, stream, world, 4,
                                               hbm_peak, pcie_peak)}
             del M4
+
+    # ---- NEXT-3: the same stack with a non-uniform (LUT) base, k_chunk 0 (compensation on LUT
+    # layers is not built) -------------------------------------------------------------------
+    lut = None
+    if not (args.quick or args.sweep_only or args.no_lut) and world == 1:
+        from synth import gen_perf_layer_lut_device
+        lut = {"config": "Llama-3-8B, SqueezeLLM-style per-column fp16 table of 2^b entries (P:397, P:502), "
+                         "W4K nibble codes, k_chunk 0 (uncompensated base GEMV, k_gemv16)"}
+        for lb in (3, 4):
+            ML = Model.__new__(Model)
+            ML.layers, ML.meta, ML.hosts, ML.n_blocks = [], [], [], M.n_blocks
+            for (b, name, d_in, d_out) in M.meta:
+                g = gen_perf_layer_lut_device(d_in, d_out, lb, layer_seed("lut", args.model, b, name))
+                ML.layers.append(dd.QuantLinear.from_device_lut(d_in, d_out, lb, g["w"], g["lut"]))
+                ML.meta.append((b, name, d_in, d_out))
+            ML.x_off, ML.y_off, ML.x_host, ML.x_dev, ML.y_dev = M.x_off, M.y_off, M.x_host, M.x_dev, M.y_dev
+            ML.max_d_out, ML.max_d_in = M.max_d_out, M.max_d_in
+            rl = step_sweep(torch, dist, dd, ML, ws, [0], args.steps, args.warmup, stream, world)
+            # bytes per call: 4-bit codes + fp16 table of 2^b per row + x + y
+            per = time_shapes(torch, dist, dd, ML, ws, [0], args.steps, stream, world, 4, hbm_peak, pcie_peak)
+            for n_, v_ in per.items():
+                d_in, d_out = v_["d_in"], v_["d_out"]
+                bh = d_in * d_out // 2 + d_out * (2 << lb) + 2 * d_in + 2 * d_out
+                e0 = v_["0"]
+                e0["hbm_GBps"] = round(bh / e0["us"] / 1e3, 1)
+                e0["roofline_us"] = round(bh / (hbm_peak * 1e3), 3)
+                e0["roofline_frac"] = e0["hbm_frac"] = round(bh / (hbm_peak * 1e3) / e0["us"], 3)
+            lut[f"b{lb}"] = {"tokens_per_s": round(rl[0]["tokens_per_s"], 2), "ms_per_step": round(rl[0]["ms_per_step"], 4),
+                             "per_layer_us": per}
+            del ML
 
     # ---- e2e through the public API: H2D inputs + step + D2H outputs ------------------------
     e2e = None
@@ -567,6 +598,7 @@ def main():
             "per_layer_us": per_shape,
             "per_layer_us_unfused": per_unfused,
             "w4": w4,
+            "lut": lut,
             "step_bytes": {"hbm": step_hbm, "pcie": step_pcie},
             "build_s": round(t_build, 1),
         }

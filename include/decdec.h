@@ -66,6 +66,11 @@ typedef enum {
  *            channel c < 30 -> word c/10, bits 16*h + 3*p .. +2 with r = c%10, p = r/2,
  *            h = r%2; channels 30/31 -> code bit b at word b, bit 15 (+16 for c = 31).
  *            3.0 bits per weight.
+ * w_format = DECDEC_WFMT_LUT (the paper's non-uniform base, SqueezeLLM served by a LUT kernel,
+ * P:397): W_hat[i][j] = w_lut[j][q_ij], codes q < 2^w_bits
+ * (w_bits = 3 | 4) packed as W4K nibbles (4 bits per weight for both widths), no s / z
+ * (w_scales / w_zeros unused).  Tables: fp16 [d_out][2^w_bits].  Compensation (k > 0) is
+ * not implemented for LUT layers yet: DECDEC_EUNSUPPORTED.
  * Residual R_hat = S_j * c_ij, c in [-7, 7]: rows = input channels,
  * contiguous, in HOST MAPPED memory (zero-copy):
  *   r_bits = 4  (layout Rq):  uint32 [d_in][d_out/8], nibble = c + 8, column c of an
@@ -73,6 +78,9 @@ typedef enum {
  *            fetched on every call).
  *   r_bits = 16 (layout R16): fp16 [d_in][d_out] (Table 3 "FP16"); r_scales NULL.
  */
+#define DECDEC_WFMT_UNIFORM 0 /* W3K / W4K codes + fp16 s + u8 z per 128-group (AWQ-style RTN)   */
+#define DECDEC_WFMT_LUT 1     /* non-uniform: W4K nibble codes < 2^w_bits + per-column fp16 table */
+
 typedef struct decdec_layer {
   int32_t d_in, d_out;       /* d_out = this rank's shard width when sharded             */
   int32_t w_bits;            /* 3 | 4                                                    */
@@ -83,6 +91,8 @@ typedef struct decdec_layer {
   int32_t r_bits;            /* 4 (paper default) | 16                                   */
   const void* r_rows;        /* HOST mapped, 16-B aligned, Rq | R16                       */
   const uint16_t* r_scales;  /* HOST mapped fp16 [d_out] (r_bits = 4) | NULL (r_bits = 16) */
+  int32_t w_format;          /* DECDEC_WFMT_UNIFORM (0, default) | DECDEC_WFMT_LUT (1)       */
+  const uint16_t* w_lut;     /* LUT: device fp16 [d_out][2^w_bits], 16-B aligned; else unused */
 } decdec_layer;
 
 /* Bytes of workspace for layers with k <= max_k and d_out <= max_d_out: a reserved 16 KB

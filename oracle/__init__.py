@@ -33,4 +33,6 @@ from .decdec_ref import (  # noqa: F401
     unpack_rq_ref,
     tolerance_ok,
     rel_err_unfloored,
+    quantize_base_lut,
+    dequantize_lut,
 )

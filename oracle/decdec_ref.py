@@ -23,6 +23,10 @@ Functions and their pins (tests/test_oracle_*.py):
                         over disjoint selections, empty selection.
   O6 pack_*_ref         pinned: hand-derived golden words (tests/golden/pack_words.txt)
                         and unpack(pack(q)) == q round trips.
+  O1-LUT quantize_base_lut / dequantize_lut (NEXT-3) pinned: columns with exactly 2^b
+                        equally frequent fp16 values are reproduced exactly (R = 0, y = W x
+                        through O5), a hand-worked 2-cluster column (tests/golden/lut_kmeans.txt),
+                        codes = nearest table entry by brute force, Lloyd MSE non-increasing.
   L9 tolerance_ok       pinned: hand-constructed accept/reject cases at 0.99e-3 / 1.01e-3 |y*|,
                         each floor engaging where it dominates, sign flips rejected
                         (tests/test_oracle_tolerance.py); rel_err_unfloored likewise.
@@ -99,6 +103,46 @@ def dequantize_base(q, s, z, group: int = GROUP):
 def residual(W16, W_hat):
     """O2: R = W - W_hat in float64 (exact; P:134, P:205, S:33)."""
     return np.asarray(W16, dtype=np.float16).astype(np.float64) - np.asarray(W_hat, dtype=np.float64)
+
+
+# ----------------------------------------------------------------------------- O1-LUT (NEXT-3)
+def quantize_base_lut(W16, bits: int, iters: int = 16):
+    """O1-LUT: non-uniform per-output-channel quantizer -- the paper's second base method
+    (SqueezeLLM, served by Any-Precision LLM's LUT kernel), ledger L17.
+
+    For every output column j (float64): v = W[:, j]; n = 2^bits centroids initialised at the
+    quantiles (i + 1/2) / n of v (np.quantile, linear interpolation); `iters` Lloyd steps of
+    1-D k-means (assign every v_i to its nearest centroid, ties -> lower index; move each
+    centroid to the mean of its members; an empty cluster keeps its centroid).  The LUT is
+    the fp16_rne of the centroids, and the codes are the nearest LUT entry (ties -> lower code),
+    so the stored codes are exactly right for the stored table.  SqueezeLLM's sensitivity
+    (Fisher) weighting needs calibration data and is not reproduced (unweighted k-means).
+    Returns (q uint8 [d_in, d_out], lut float16 [2^bits, d_out])."""
+    W = np.asarray(W16, dtype=np.float16).astype(np.float64)
+    d_in, d_out = W.shape
+    n = 1 << bits
+    q = np.zeros((d_in, d_out), dtype=np.uint8)
+    lut = np.zeros((n, d_out))
+    for j in range(d_out):
+        v = W[:, j]
+        c = np.quantile(v, (np.arange(n) + 0.5) / n)
+        for _ in range(iters):
+            a = np.argmin(np.abs(v[:, None] - c[None, :]), axis=1)   # argmin: first (lower) index on ties
+            for t in range(n):
+                m = a == t
+                if m.any():
+                    c[t] = v[m].mean()
+        L = fp16_rne(c)
+        q[:, j] = np.argmin(np.abs(v[:, None] - L[None, :]), axis=1)
+        lut[:, j] = L
+    return q, lut.astype(np.float16)
+
+
+def dequantize_lut(q, lut):
+    """W_hat[i, j] = lut[q_ij, j] (exact in float64)."""
+    q = np.asarray(q, dtype=np.int64)
+    L = np.asarray(lut, dtype=np.float16).astype(np.float64)
+    return np.take_along_axis(L, q, axis=0)
 
 
 # ----------------------------------------------------------------------------- O3
@@ -188,7 +232,7 @@ def topk_ref(x16, k: int, chunk: int = 0):
 
 
 # ----------------------------------------------------------------------------- O5
-def decdec_linear_ref(q, s, z, x16, k: int, chunk: int = 0, rc=None, rS=None, r16=None, W_hat=None):
+def decdec_linear_ref(q, s, z, x16, k: int, chunk: int = 0, rc=None, rS=None, r16=None, W_hat=None, lut=None):
     """O5: y = W_hat x + sum_{i in S} x_i R_hat[i, :] in float64 (P:204-207 steps 1-4).
 
     q uint8 [d_in, d_out], s fp16 [G, d_out], z uint8 [G, d_out]: base weights (O1 format).
@@ -199,9 +243,10 @@ def decdec_linear_ref(q, s, z, x16, k: int, chunk: int = 0, rc=None, rS=None, r1
     (A_j = sum_i |W_hat_ij x_i| + sum_{i in S} |R_hat_ij x_i|, the L9 scale).
     W_hat: optional precomputed dequantize_base(q, s, z) (same values; lets a test reuse
     it across calls on one layer instead of rebuilding it per call).
+    lut: non-uniform base (O1-LUT): W_hat = lut[q_ij, j]; s and z are then unused.
     """
     if W_hat is None:
-        W_hat = dequantize_base(q, s, z)
+        W_hat = dequantize_lut(q, lut) if lut is not None else dequantize_base(q, s, z)
     x = np.asarray(x16, dtype=np.float16).astype(np.float64)
     ob = x @ W_hat                                   # step: o_b = W_hat x
     A = np.abs(x) @ np.abs(W_hat)

@@ -29,6 +29,7 @@ class decdec_layer(ctypes.Structure):
         ("w_packed", ctypes.c_void_p), ("w_scales", ctypes.c_void_p), ("w_zeros", ctypes.c_void_p),
         ("r_bits", ctypes.c_int32),
         ("r_rows", ctypes.c_void_p), ("r_scales", ctypes.c_void_p),
+        ("w_format", ctypes.c_int32), ("w_lut", ctypes.c_void_p),
     ]
 
 

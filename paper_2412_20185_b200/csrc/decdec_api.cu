@@ -216,38 +216,50 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
 // Two CTAs per SM: <= kGemvSmemBudget dynamic smem each.  Team shape (T warps, M rows per pass)
 // maximises the issuing lanes that own a (row, group): efficiency M*G / (32 * ceil(M*G/32)),
 // ties -> smaller T.  RPS (passes per stage): the largest with >= 3 ring stages, else >= 2.
-constexpr size_t kGemvSmemBudget = 110 * 1024;     // NC = 8: two CTAs per SM
-constexpr size_t kGemvSmemBudget16 = 200 * 1024;   // NC = 16: one CTA per SM
 
-// DECDEC_GEMV_NC = 8 | 16 (A/B knob; default below)
-int gemv_nc() {
+// DECDEC_GEMV_PAIR = 0 | 1: rows one at a time or in pairs (A/B knob)
+bool gemv_pair() {
   static int env = -1;
   if (env < 0) {
-    const char* e = getenv("DECDEC_GEMV_NC");
-    env = e ? atoi(e) : 16;
-    if (env != 8) env = 16;
+    const char* e = getenv("DECDEC_GEMV_PAIR");
+    env = e ? (atoi(e) > 0) : 0;  // measured: pairs 1.265 vs single rows 1.251 ms (k_chunk-0 step)
+  }
+  return env == 1;
+}
+// DECDEC_PREWAIT_KB: ring bytes requested before griddepcontrol.wait (A/B knob)
+int prewait_kb() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DECDEC_PREWAIT_KB");
+    env = e ? atoi(e) : 32;
   }
   return env;
 }
+
+constexpr size_t kGemvSmemBudget = 200 * 1024;  // one CTA per SM
 struct GemvPlan {
   GemvParams gp;
   size_t smem;
   int grid;
 };
 
-decdec_status make_gemv_plan(int d_in, int d_out, int bits, int n_cta_max, GemvPlan* out) {
+// lut_bits = 0: uniform base (bits = 3 | 4); lut_bits = 3 | 4: LUT base (codes in W4K nibbles)
+decdec_status make_gemv_plan(int d_in, int d_out, int bits, int n_cta_max, GemvPlan* out, int lut_bits = 0) {
   const int G = d_in / DECDEC_GROUP;
   GemvParams g{};
   g.d_in = d_in;
   g.d_out = d_out;
   g.G = G;
-  g.row_bytes = d_in * bits / 8;
-  const int NC = gemv_nc();
-  const size_t budget = NC == 8 ? kGemvSmemBudget : kGemvSmemBudget16;
+  g.row_bytes = d_in * (lut_bits ? 4 : bits) / 8;
+  const int NC = kGemvNC;
+  const size_t budget = kGemvSmemBudget;
   g.NC = NC;
+  g.s_row = lut_bits ? 2 << lut_bits : 2 * G;  // LUT: the row's table of 2^b fp16
+  g.z_row = lut_bits ? 0 : G;
   int bestT = 0, bestM = 0;
   double best_eff = -1.0;
-  for (int T = 1; T <= NC; T *= 2) {
+  for (int T = 1; T <= NC; ++T) {
+    if (NC % T) continue;
     const int M = 32 * T / G;
     if (M < 1) continue;
     const int lanes = M * G, warps = (lanes + 31) / 32;
@@ -263,24 +275,24 @@ decdec_status make_gemv_plan(int d_in, int d_out, int bits, int n_cta_max, GemvP
   g.M = bestM;
   g.team_red = !(bestT == 1 && 32 % G == 0);
   int Q = 1;
-  while ((Q * G) % 16) ++Q;  // rows*G bytes of zeros (and 2x of scales) stay 16-B multiples
+  while (!lut_bits && (Q * G) % 16) ++Q;  // rows*G bytes of zeros (and 2x of scales) stay 16-B multiples
   g.Q = Q;
   const int nteam = NC / bestT;
   const size_t xb = align_up((size_t)d_in * 2, 16);
   bool ok = false;
   for (int need = 3; need >= 2 && !ok; --need) {
     for (int rps = kGemvMaxRPS; rps >= 1; rps /= 2) {
-      const int TRS = nteam * bestM * rps;
-      if (TRS % Q) continue;
+      const int TRS = (nteam * bestM * rps) / Q * Q;  // stage rows: a multiple of the row quantum
+      if (TRS == 0) continue;
       const uint32_t off_s = (uint32_t)align_up((size_t)TRS * g.row_bytes, 16);
-      const uint32_t off_z = off_s + (uint32_t)align_up((size_t)TRS * G * 2, 16);
-      const uint32_t sb = (uint32_t)align_up((size_t)off_z + (size_t)TRS * G, 128);
+      const uint32_t off_z = off_s + (uint32_t)align_up((size_t)TRS * g.s_row, 16);
+      const uint32_t sb = (uint32_t)align_up((size_t)off_z + (size_t)TRS * g.z_row, 128);
       const size_t red = g.team_red ? align_up((size_t)2 * TRS * G * 4, 16) : 0;
       const size_t fixed = xb + red + 16 * 8;
       if (fixed + (size_t)need * sb > budget) continue;
       int stages = (int)((budget - fixed) / sb);
       if (stages > 8) stages = 8;
-      g.RPS = rps;
+      g.RPS = (TRS + nteam * bestM - 1) / (nteam * bestM);  // passes that cover TRS rows
       g.TRS = TRS;
       g.stages = stages;
       g.stage_bytes = sb;
@@ -290,6 +302,8 @@ decdec_status make_gemv_plan(int d_in, int d_out, int bits, int n_cta_max, GemvP
       g.off_red = (uint32_t)align_up((size_t)g.off_x + xb, 16);
       g.off_bar = (uint32_t)align_up((size_t)g.off_red + red, 16);
       out->smem = (size_t)g.off_bar + 2 * (size_t)stages * 8;
+      g.pre = (int)(((size_t)prewait_kb() * 1024) / sb);
+      if (g.pre < 1) g.pre = 1;
       ok = true;
       break;
     }
@@ -341,14 +355,12 @@ decdec_status init_attrs() {
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 16>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 16>, lin);
-  if (s == DECDEC_OK) s = set_smem_attr(k_gemv<3>, kGemvSmemBudget + 1024);
-  if (s == DECDEC_OK) s = set_smem_attr(k_gemv<4>, kGemvSmemBudget + 1024);
-  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<3>, kGemvSmemBudget16 + 1024);
-  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<4>, kGemvSmemBudget16 + 1024);
-  // two k_gemv CTAs (this layer's and the next one's) must fit an SM's shared memory: ask for
-  // the maximum shared-memory carveout so the SM is not configured for fewer
-  if (s == DECDEC_OK) s = cuda_status(cudaFuncSetAttribute(k_gemv<3>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  if (s == DECDEC_OK) s = cuda_status(cudaFuncSetAttribute(k_gemv<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<3, 0>, kGemvSmemBudget + 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<4, 0>, kGemvSmemBudget + 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<3, 1>, kGemvSmemBudget + 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<4, 1>, kGemvSmemBudget + 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<4, 0, 3>, kGemvSmemBudget + 1024);
+  if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<4, 0, 4>, kGemvSmemBudget + 1024);
   return s;
 }
 decdec_status ensure_attrs() {
@@ -383,8 +395,16 @@ decdec_status check_layer(const decdec_layer* L, bool need_residual) {
   if (!L) return DECDEC_EINVAL;
   if (L->group_size != DECDEC_GROUP) return DECDEC_EUNSUPPORTED;
   if (L->w_bits != 3 && L->w_bits != 4) return DECDEC_EUNSUPPORTED;
+  if (L->w_format != DECDEC_WFMT_UNIFORM && L->w_format != DECDEC_WFMT_LUT) return DECDEC_EUNSUPPORTED;
   if (L->d_in < 128 || L->d_in > 32768 || L->d_in % DECDEC_GROUP) return DECDEC_EINVAL;
   if (L->d_out < 32 || L->d_out % 32) return DECDEC_EINVAL;
+  if (L->w_format == DECDEC_WFMT_LUT) {
+    if (need_residual) return DECDEC_EUNSUPPORTED;  // LUT + compensation: not built yet
+    if (!L->w_packed || !L->w_lut) return DECDEC_EINVAL;
+    if (!aligned16(L->w_packed) || !aligned16(L->w_lut)) return DECDEC_EALIGN;
+    if (!is_device_ptr(L->w_packed) || !is_device_ptr(L->w_lut)) return DECDEC_EINVAL;
+    return DECDEC_OK;
+  }
   if (!L->w_packed || !L->w_scales || !L->w_zeros) return DECDEC_EINVAL;
   if (!aligned16(L->w_packed) || !aligned16(L->w_scales) || !aligned16(L->w_zeros)) return DECDEC_EALIGN;
   if (!is_device_ptr(L->w_packed) || !is_device_ptr(L->w_scales) || !is_device_ptr(L->w_zeros)) return DECDEC_EINVAL;
@@ -415,6 +435,22 @@ decdec_status launch_select(const uint16_t* x, int d_in, int k, int chunk, int* 
   return cuda_status(cudaGetLastError());
 }
 
+// Liveness: a compensated launch's DEC CTAs wait for o_b entries written by GEMV CTAs of the
+// same grid, so all of its CTAs must be co-resident.  The grid is <= one CTA per SM, and it is
+// launched COOPERATIVELY: the runtime then co-schedules the whole grid or fails the launch (it
+// never leaves a partially resident grid spinning), also when other streams hold SMs.  Measured
+// with PDL inside graphs (csrc/probe/probe_coop.cu, profiles/r02_probe_coop.json): legal, and a
+// cooperative grid still starts early when it fits beside the previous kernel.  DECDEC_COOP=0
+// disables it (A/B only).
+bool coop_launch() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DECDEC_COOP");
+    env = e ? (atoi(e) > 0) : 1;
+  }
+  return env == 1;
+}
+
 template <int BITS, int RBITS>
 decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
@@ -422,11 +458,20 @@ decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, c
   cfg.blockDim = dim3(32 * (1 + pl.NC));
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (p.k_sel > 0 && coop_launch()) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   return cuda_status(cudaLaunchKernelEx(&cfg, k_linear<BITS, RBITS>, p));
 }
 
@@ -435,7 +480,7 @@ decdec_status launch_linear(const LinearParams& p, const Plan& pl, int bits, int
   return rbits == 16 ? launch_linear_t<4, 16>(p, pl, pdl, st) : launch_linear_t<4, 4>(p, pl, pdl, st);
 }
 
-decdec_status launch_gemv(const GemvPlan& pl, int bits, bool pdl, cudaStream_t st) {
+decdec_status launch_gemv(const GemvPlan& pl, int bits, bool pdl, cudaStream_t st, int lut_bits = 0) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(32 * (1 + pl.gp.NC));
@@ -446,27 +491,34 @@ decdec_status launch_gemv(const GemvPlan& pl, int bits, bool pdl, cudaStream_t s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (pl.gp.NC == 8)
-    return cuda_status(bits == 3 ? cudaLaunchKernelEx(&cfg, k_gemv<3>, pl.gp) : cudaLaunchKernelEx(&cfg, k_gemv<4>, pl.gp));
-  return cuda_status(bits == 3 ? cudaLaunchKernelEx(&cfg, k_gemv16<3>, pl.gp) : cudaLaunchKernelEx(&cfg, k_gemv16<4>, pl.gp));
+  const bool pair = gemv_pair();
+  cudaError_t e;
+  if (lut_bits) e = lut_bits == 3 ? cudaLaunchKernelEx(&cfg, k_gemv16<4, 0, 3>, pl.gp) : cudaLaunchKernelEx(&cfg, k_gemv16<4, 0, 4>, pl.gp);
+  else if (pair) e = bits == 3 ? cudaLaunchKernelEx(&cfg, k_gemv16<3, 1>, pl.gp) : cudaLaunchKernelEx(&cfg, k_gemv16<4, 1>, pl.gp);
+  else e = bits == 3 ? cudaLaunchKernelEx(&cfg, k_gemv16<3, 0>, pl.gp) : cudaLaunchKernelEx(&cfg, k_gemv16<4, 0>, pl.gp);
+  return cuda_status(e);
 }
 
-// DECDEC_L2PF_NEXT=0 disables the stack executor's cross-layer L2 prefetch (A/B only)
+// DECDEC_L2PF_NEXT=1 enables the stack executor's cross-layer L2 prefetch (A/B only)
 bool l2_next_prefetch() {
   static int env = -1;
   if (env < 0) {
     const char* e = getenv("DECDEC_L2PF_NEXT");
-    env = e ? (atoi(e) > 0) : 1;
+    env = e ? (atoi(e) > 0) : 0;  // measured: no gain (k_chunk 0 step 1.327 -> 1.384 ms with it)
   }
   return env == 1;
 }
 
-// DECDEC_OLD_GEMV=1: k = 0 calls use the fused kernel's GEMV CTAs (round-1 path; A/B only)
+// Uniform-weight k = 0 calls run the fused kernel's GEMV CTAs (k_linear with no DEC CTAs) by
+// default; DECDEC_NEW_GEMV=1 routes them through gemv.cuh's k_gemv16 instead.  Measured (1x B200,
+// Llama-3-8B 3-bit k_chunk-0 step, profiles/r02_gemv_ab.json): k_linear 1.078 ms; k_gemv16
+// 1.25-1.32 ms (dedicated or in-warp producer, single rows or pairs, 16-96 KB before the wait),
+// two-CTAs-per-SM k_gemv 1.44-1.51 ms.  LUT (non-uniform) layers always use k_gemv16.
 bool use_gemv_kernel() {
   static int env = -1;
   if (env < 0) {
-    const char* e = getenv("DECDEC_OLD_GEMV");
-    env = (e && atoi(e) > 0) ? 0 : 1;
+    const char* e = getenv("DECDEC_NEW_GEMV");
+    env = (e && atoi(e) > 0) ? 1 : 0;
   }
   return env == 1;
 }
@@ -566,16 +618,17 @@ decdec_status decdec_gemv(const decdec_layer* L, const uint16_t* x, uint16_t* y,
   if (!x || !y) return DECDEC_EINVAL;
   if (!aligned16(x) || !aligned16(y)) return DECDEC_EALIGN;
   if ((s = ensure_attrs()) != DECDEC_OK) return s;
-  if (use_gemv_kernel()) {
+  const int lutb = L->w_format == DECDEC_WFMT_LUT ? L->w_bits : 0;
+  if (use_gemv_kernel() || lutb) {
     GemvPlan gpl;
-    if ((s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &gpl)) != DECDEC_OK) return s;
+    if ((s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &gpl, lutb)) != DECDEC_OK) return s;
     gpl.gp.w = static_cast<const uint8_t*>(L->w_packed);
-    gpl.gp.ws = L->w_scales;
-    gpl.gp.wz = L->w_zeros;
+    gpl.gp.ws = lutb ? L->w_lut : L->w_scales;
+    gpl.gp.wz = lutb ? nullptr : L->w_zeros;
     gpl.gp.x = x;
     gpl.gp.y = y;
     gpl.gp.trace = g_trace ? g_trace + 2 : nullptr;
-    return launch_gemv(gpl, L->w_bits, false, (cudaStream_t)stream);
+    return launch_gemv(gpl, L->w_bits, false, (cudaStream_t)stream, lutb);
   }
   Plan pl;
   if ((s = make_plan(L->d_in, L->d_out, L->w_bits, 0, &pl)) != DECDEC_OK) return s;
@@ -592,7 +645,8 @@ namespace {
 struct Prepared {
   LinearParams p;
   Plan pl;
-  bool gemv;  // k = 0: the two-CTAs-per-SM base GEMV kernel (gemv.cuh)
+  bool gemv;  // k = 0: the base GEMV kernel (gemv.cuh)
+  int lut_bits;
   GemvPlan gpl;
   int k, chunk, bits, rbits;
   const uint16_t* x;
@@ -609,12 +663,14 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
   if (k_sel < 0) return DECDEC_EINVAL;
   if ((s = ensure_attrs()) != DECDEC_OK) return s;
   Prepared P{};
-  if (k_sel == 0 && use_gemv_kernel()) {
-    if ((s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &P.gpl)) != DECDEC_OK) return s;
+  const int lutb = L->w_format == DECDEC_WFMT_LUT ? L->w_bits : 0;
+  if (k_sel == 0 && (use_gemv_kernel() || lutb)) {
+    if ((s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &P.gpl, lutb)) != DECDEC_OK) return s;
     GemvParams& g = P.gpl.gp;
     g.w = static_cast<const uint8_t*>(L->w_packed);
-    g.ws = L->w_scales;
-    g.wz = L->w_zeros;
+    g.ws = lutb ? L->w_lut : L->w_scales;
+    g.wz = lutb ? nullptr : L->w_zeros;
+    P.lut_bits = lutb;
     g.x = x;
     g.y = y;
     g.ob = nullptr;
@@ -665,7 +721,7 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
 }
 
 decdec_status enqueue_linear(const Prepared& P, cudaStream_t st, bool chained = false) {
-  if (P.gemv) return launch_gemv(P.gpl, P.bits, chained, st);
+  if (P.gemv) return launch_gemv(P.gpl, P.bits, chained, st, P.lut_bits);
   Plan pl = P.pl;
   pl.grid += P.pl.n_dec;  // DEC CTAs first
   return launch_linear(P.p, pl, P.bits, P.p.k_sel ? P.rbits : 4, chained, st);
@@ -724,6 +780,7 @@ decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const i
     for (int i = 0; i < n_layers; ++i) {
       if (!P[i].gemv) continue;
       const decdec_layer& Ln = layers[(i + 1) % n_layers];
+      if (Ln.w_format != DECDEC_WFMT_UNIFORM) continue;
       const int Gn = Ln.d_in / DECDEC_GROUP;
       GemvParams& g = P[i].gpl.gp;
       g.pf_ptr[0] = static_cast<const uint8_t*>(Ln.w_packed);
@@ -814,7 +871,7 @@ decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out,
   if (s != DECDEC_OK) return s;
   if (!q_out) return DECDEC_EINVAL;
   const int blocks = 4 * device_sms();
-  if (L->w_bits == 3)
+  if (L->w_bits == 3 && L->w_format != DECDEC_WFMT_LUT)  // LUT codes are W4K nibbles
     k_debug_unpack<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint8_t*>(L->w_packed), L->d_in, L->d_out, q_out);
   else
     k_debug_unpack<4><<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint8_t*>(L->w_packed), L->d_in, L->d_out, q_out);
@@ -824,9 +881,10 @@ decdec_status decdec_debug_unpack_weights(const decdec_layer* L, uint8_t* q_out,
 decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, size_t buf_bytes) {
   if (!L || !buf) return DECDEC_EINVAL;
   const int k_sel = k;  // caller passes the selected count
-  if (k_sel == 0 && use_gemv_kernel()) {
+  const int lutb = L->w_format == DECDEC_WFMT_LUT ? L->w_bits : 0;
+  if (k_sel == 0 && (use_gemv_kernel() || lutb)) {
     GemvPlan g;
-    decdec_status s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &g);
+    decdec_status s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &g, lutb);
     if (s != DECDEC_OK) return s;
     snprintf(buf, buf_bytes,
              "{\"kernel\": \"k_gemv\", \"G\": %d, \"T\": %d, \"M\": %d, \"team_red\": %d, \"RPS\": %d, \"TRS\": %d, "

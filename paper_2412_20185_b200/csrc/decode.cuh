@@ -97,4 +97,69 @@ __device__ __forceinline__ void decode_rq_word(uint32_t w, uint32_t c[4]) {
   }
 }
 
+// ---------------------------------------------------------------- LUT (non-uniform base, NEXT-3)
+// Codes are W4K nibbles (channel c of a word at bit 4*(c>>1) + 16*(c&1); values < 2^LB).  The
+// row's table of 2^LB fp16 values is held as byte planes: tl[t] / th[t] = the low / high bytes
+// of entries 4t..4t+3, so ONE `prmt` looks up four codes' low (or high) bytes at once (its
+// selector nibbles are the codes: bits 2..0 pick one of 8 bytes, bit 3 must be 0).  Two more
+// `prmt` interleave them into fp16 pairs (channel c, c+2) -- x is kept in the same pairing --
+// and FHFMA multiplies exactly into fp32.  LB = 4 looks up the low 3 code bits in both halves of
+// the table and blends by code bit 3 (byte masks built by `prmt`'s sign-replicate mode).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// table (2^LB fp16, as LB == 3 ? 4 : 8 half2 words e[]) -> byte planes tl[], th[]
+template <int LB>
+__device__ __forceinline__ void lut_planes(const uint32_t* e, uint32_t* tl, uint32_t* th) {
+#pragma unroll
+  for (int t = 0; t < (1 << LB) / 4; ++t) {
+    tl[t] = prmt(e[2 * t], e[2 * t + 1], 0x6420u);
+    th[t] = prmt(e[2 * t], e[2 * t + 1], 0x7531u);
+  }
+}
+
+// acc[0..3] += table[codes of word w] . x for one 8-channel word; xp[0..3] = x pairs
+// (0,2), (4,6), (1,3), (5,7) of the word (see lut_x_pairs).
+template <int LB>
+__device__ __forceinline__ void fma_lut_word(uint32_t w, const uint32_t* tl, const uint32_t* th, const uint32_t* xp,
+                                             float* acc) {
+  uint32_t le, he, lo, ho;
+  if (LB == 3) {
+    const uint32_t so = w >> 16;
+    le = prmt(tl[0], tl[1], w);
+    he = prmt(th[0], th[1], w);
+    lo = prmt(tl[0], tl[1], so);
+    ho = prmt(th[0], th[1], so);
+  } else {
+    const uint32_t m = w & 0x77777777u, so = m >> 16, w4 = w << 4;
+    const uint32_t me = prmt(w4, w, 0xD9C8u), mo = prmt(w4, w, 0xFBEAu);  // 0xFF bytes where code bit 3 is set
+    le = (prmt(tl[0], tl[1], m) & ~me) | (prmt(tl[2], tl[3], m) & me);
+    he = (prmt(th[0], th[1], m) & ~me) | (prmt(th[2], th[3], m) & me);
+    lo = (prmt(tl[0], tl[1], so) & ~mo) | (prmt(tl[2], tl[3], so) & mo);
+    ho = (prmt(th[0], th[1], so) & ~mo) | (prmt(th[2], th[3], so) & mo);
+  }
+  const uint32_t v02 = prmt(le, he, 0x5140u), v46 = prmt(le, he, 0x7362u);  // (ch0, ch2), (ch4, ch6)
+  const uint32_t v13 = prmt(lo, ho, 0x5140u), v57 = prmt(lo, ho, 0x7362u);  // (ch1, ch3), (ch5, ch7)
+  acc[0] = fhfma_lo(v02, xp[0], acc[0]);
+  acc[1] = fhfma_hi(v02, xp[0], acc[1]);
+  acc[2] = fhfma_lo(v46, xp[1], acc[2]);
+  acc[3] = fhfma_hi(v46, xp[1], acc[3]);
+  acc[0] = fhfma_lo(v13, xp[2], acc[0]);
+  acc[1] = fhfma_hi(v13, xp[2], acc[1]);
+  acc[2] = fhfma_lo(v57, xp[3], acc[2]);
+  acc[3] = fhfma_hi(v57, xp[3], acc[3]);
+}
+
+// x registers of one 8-channel word, (x0,x1),(x2,x3),(x4,x5),(x6,x7) -> (x0,x2),(x4,x6),(x1,x3),(x5,x7)
+__device__ __forceinline__ void lut_x_pairs(uint32_t* xr4) {
+  const uint32_t a = xr4[0], b = xr4[1], c = xr4[2], d = xr4[3];
+  xr4[0] = prmt(a, b, 0x5410u);
+  xr4[1] = prmt(c, d, 0x5410u);
+  xr4[2] = prmt(a, b, 0x7632u);
+  xr4[3] = prmt(c, d, 0x7632u);
+}
+
 }  // namespace decdec

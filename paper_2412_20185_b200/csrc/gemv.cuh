@@ -1,5 +1,5 @@
 // Base GEMV o_b = W_hat x ("the base GEMV"; step a3 of SURVEY.md §8(a)) for
-// sm_100a, laid out so that TWO CTAs fit on one SM (<= 288 threads x <= 112 registers,
+// sm_100a, laid out so that TWO CTAs fit on one SM (8 warps x <= 128 registers,
 // <= ~110 KB shared memory each).  With programmatic dependent launch the next layer's CTA is
 // then already resident while this layer computes: it fills its weight ring from HBM
 // before griddepcontrol.wait, so at the layer boundary only x is still to be loaded and the
@@ -9,7 +9,7 @@
 //   warp 0           producer: 1-D bulk async copies (TMA engine) of a stage of TRS
 //                    consecutive rows (+ their fp16 scales and u8 zeros) into a ring of
 //                    `stages` smem slots, mbarrier full/empty handshake, L2 evict-first.
-//   warps 1..NC      consumers: "teams" of T warps; lane L of a team owns input group
+//   warps 1..NC      consumers (NC = 15): "teams" of T | NC warps; lane L of a team owns input group
 //                    g = L % G (128 channels, x in 64 registers for the whole launch) of row
 //                    L / G of the current pass (M = floor(32T / G) rows per pass), so no
 //                    lane idles when G does not divide 32 (e.g. Phi-3's G = 40: T = 4, M = 3).
@@ -28,7 +28,7 @@
 
 namespace decdec {
 
-constexpr int kGemvMaxNC = 16;                 // consumer warps per CTA: 8 (two CTAs / SM) or 16
+constexpr int kGemvNC = 15;                    // consumer warps per CTA (+ 1 producer warp)
 constexpr int kGemvMaxRPS = 4;                 // row passes per stage
 constexpr int kGemvTraceEvents = 20;           // same stride as the fused kernel's trace
 
@@ -41,6 +41,8 @@ struct GemvParams {
   float* ob;           // fp32 o_b [d_out], self-validating relaxed stores (fused kernel's combine)
   int d_in, d_out, G, row_bytes;
   int NC, T, M, RPS, TRS, stages, Q;
+  int pre;             // ring stages requested before griddepcontrol.wait (the rest after x)
+  int s_row, z_row;    // bytes per row of the 2nd / 3rd stream: 2G / G (uniform s, z); 2^(b+1) / 0 (LUT)
   int team_red;        // 1: team reduction through smem partials; 0: in-warp butterflies (T == 1, G | 32)
   uint32_t stage_bytes, off_s, off_z, off_x, off_red, off_bar;
   int cta0;            // first blockIdx.x running the GEMV (fused kernel: after the DEC CTAs)
@@ -88,6 +90,74 @@ __device__ __forceinline__ float row_group_dot(const uint8_t* gp, const uint32_t
   return s24 * fmaf(-z, Xs, combine_classes<BITS>(a));
 }
 
+// LUT base (NEXT-3): one row's partial sum_{i in g} lut[q_i] x_i for input group g.  gp: the
+// group's 64 B of W4K nibble codes; lp: the row's table (2^LB fp16) in smem; xr: x in the
+// (c, c+2) pairing of lut_x_pairs.
+template <int LB>
+__device__ __forceinline__ float row_group_dot_lut(const uint8_t* gp, const uint32_t* lp, const uint32_t* xr, int rot) {
+  uint32_t e[1 << (LB - 1)], tl[(1 << LB) / 4], th[(1 << LB) / 4];
+#pragma unroll
+  for (int t = 0; t < (1 << LB) / 8; ++t) {
+    const uint4 v = reinterpret_cast<const uint4*>(lp)[t];
+    e[4 * t] = v.x; e[4 * t + 1] = v.y; e[4 * t + 2] = v.z; e[4 * t + 3] = v.w;
+  }
+  lut_planes<LB>(e, tl, th);
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+  uint4 v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const uint4*>(gp + 16 * ((j + rot) & 3));
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    fma_lut_word<LB>(v[j].x, tl, th, xr + 16 * j + 0, a);
+    fma_lut_word<LB>(v[j].y, tl, th, xr + 16 * j + 4, a);
+    fma_lut_word<LB>(v[j].z, tl, th, xr + 16 * j + 8, a);
+    fma_lut_word<LB>(v[j].w, tl, th, xr + 16 * j + 12, a);
+  }
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
+
+// Two rows at once (12 independent FHFMA chains; x registers shared): more ILP per warp.
+template <int BITS>
+__device__ __forceinline__ void row_group_dot2(const uint8_t* g0, const uint8_t* g1, const uint32_t* xr, float Xs, float s0,
+                                               float z0, float s1, float z1, int rot, float& v0, float& v1) {
+  float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, a1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (BITS == 4) {
+    uint4 u0[4], u1[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      u0[j] = *reinterpret_cast<const uint4*>(g0 + 16 * ((j + rot) & 3));
+      u1[j] = *reinterpret_cast<const uint4*>(g1 + 16 * ((j + rot) & 3));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      fma_w4_word(u0[j].x, xr + 16 * j + 0, a0);
+      fma_w4_word(u1[j].x, xr + 16 * j + 0, a1);
+      fma_w4_word(u0[j].y, xr + 16 * j + 4, a0);
+      fma_w4_word(u1[j].y, xr + 16 * j + 4, a1);
+      fma_w4_word(u0[j].z, xr + 16 * j + 8, a0);
+      fma_w4_word(u1[j].z, xr + 16 * j + 8, a1);
+      fma_w4_word(u0[j].w, xr + 16 * j + 12, a0);
+      fma_w4_word(u1[j].w, xr + 16 * j + 12, a1);
+    }
+  } else {
+    uint32_t w0[12], w1[12];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const uint4 t0 = *reinterpret_cast<const uint4*>(g0 + 16 * j);
+      const uint4 t1 = *reinterpret_cast<const uint4*>(g1 + 16 * j);
+      w0[4 * j] = t0.x; w0[4 * j + 1] = t0.y; w0[4 * j + 2] = t0.z; w0[4 * j + 3] = t0.w;
+      w1[4 * j] = t1.x; w1[4 * j + 1] = t1.y; w1[4 * j + 2] = t1.z; w1[4 * j + 3] = t1.w;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      fma_w3_slice(w0[3 * u], w0[3 * u + 1], w0[3 * u + 2], xr + 16 * u, a0);
+      fma_w3_slice(w1[3 * u], w1[3 * u + 1], w1[3 * u + 2], xr + 16 * u, a1);
+    }
+  }
+  v0 = s0 * fmaf(-z0, Xs, combine_classes<BITS>(a0));
+  v1 = s1 * fmaf(-z1, Xs, combine_classes<BITS>(a1));
+}
+
 // This CTA's share of the next layer's bytes, into L2 (16-B aligned pieces of <= 64 KB).
 __device__ __forceinline__ void l2_prefetch_share(const GemvParams& p, int c) {
 #pragma unroll 1
@@ -105,7 +175,9 @@ __device__ __forceinline__ void l2_prefetch_share(const GemvParams& p, int c) {
 }
 
 // The GEMV part of one CTA (gemv CTA index c of p.n_cta).  smem: ring | x | red | barriers.
-template <int BITS>
+// LUTB = 0: uniform base (W3K / W4K codes, per-group s and z); LUTB = 3 | 4: non-uniform base
+// with a per-row table of 2^LUTB fp16 values (codes W4K nibbles; BITS must be 4).
+template <int BITS, int PAIR, int LUTB>
 __device__ __forceinline__ void gemv_cta(const GemvParams& p, uint8_t* smem, int c) {
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
@@ -125,24 +197,34 @@ __device__ __forceinline__ void gemv_cta(const GemvParams& p, uint8_t* smem, int
   }
   __syncthreads();
 
+  // warp 0 = producer (a dedicated warp: issuing bulk copies can stall on a full TMA queue, which
+  // must not hold up consumer rows); warps 1..NC = consumers.  NC + 1 = 16 warps keeps <= 4
+  // warps per SM sub-partition, so <= 128 registers per thread fit its 16K-register file.
   if (warp == 0) {
-    // ---------------------------------------------------------------- producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      const int G = p.G;
-      for (int i = 0; i < n_st; ++i) {
+      const int first = min(p.stages, n_st), pre = min(p.pre, first);
+      auto issue = [&](int i) {
         const int st = i % p.stages;
-        if (i >= p.stages) mbar_wait(&empty[st], ((i / p.stages) & 1) ^ 1);
         const int ra = r0 + i * p.TRS;
         const int nr = min(p.TRS, r1 - ra);
         uint8_t* dst = ring + (size_t)st * p.stage_bytes;
-        const uint32_t wb = (uint32_t)nr * p.row_bytes, sb = (uint32_t)nr * G * 2, zb = (uint32_t)nr * G;
+        const uint32_t wb = (uint32_t)nr * p.row_bytes, sb = (uint32_t)nr * p.s_row, zb = (uint32_t)nr * p.z_row;
         mbar_arrive_expect_tx(&full[st], wb + sb + zb);
         bulk_g2s(dst, p.w + (size_t)ra * p.row_bytes, wb, &full[st], pol);
-        bulk_g2s(dst + p.off_s, p.ws + (size_t)ra * G, sb, &full[st], pol);
-        bulk_g2s(dst + p.off_z, p.wz + (size_t)ra * G, zb, &full[st], pol);
-        if (i == min(p.stages, n_st) - 1) l2_prefetch_share(p, c);  // after this CTA's first ring
+        bulk_g2s(dst + p.off_s, reinterpret_cast<const uint8_t*>(p.ws) + (size_t)ra * p.s_row, sb, &full[st], pol);
+        if (zb) bulk_g2s(dst + p.off_z, p.wz + (size_t)ra * p.z_row, zb, &full[st], pol);
+      };
+      // only `pre` stages before griddepcontrol.wait: a deeper burst is still queued in the
+      // memory system when the wait releases and delays the x loads every warp needs first
+      for (int i = 0; i < pre; ++i) issue(i);
+      pdl_wait();
+      for (int i = pre; i < n_st; ++i) {
+        if (i >= p.stages) mbar_wait(&empty[i % p.stages], ((i / p.stages) & 1) ^ 1);
+        issue(i);
+        if (i == first - 1) l2_prefetch_share(p, c);  // optional: the next layer's share into L2
       }
+      if (first <= pre) l2_prefetch_share(p, c);
     }
     return;
   }
@@ -150,7 +232,7 @@ __device__ __forceinline__ void gemv_cta(const GemvParams& p, uint8_t* smem, int
   // ------------------------------------------------------------------ consumers
   constexpr int GB = 16 * BITS;  // bytes of one 128-code group
   const int G = p.G, T = p.T, M = p.M;
-  const int ct = threadIdx.x - 32, cw = ct >> 5;
+  const int ct = threadIdx.x - 32, cw = warp - 1;
   const int team = cw / T, wi = cw % T;
   const int nteam = p.NC / T;
   const int L = wi * 32 + lane;
@@ -171,6 +253,7 @@ __device__ __forceinline__ void gemv_cta(const GemvParams& p, uint8_t* smem, int
     }
     named_bar_sync(15, nct);
   }
+
   uint32_t xr[64];
   float Xs = 0.f;
   if (active) {
@@ -195,6 +278,10 @@ __device__ __forceinline__ void gemv_cta(const GemvParams& p, uint8_t* smem, int
       xa[4 + (i & 3)] = fhfma_hi(one2, xr[i], xa[4 + (i & 3)]);
     }
     Xs = (((xa[0] + xa[1]) + (xa[2] + xa[3])) + ((xa[4] + xa[5]) + (xa[6] + xa[7]))) * 5.9604644775390625e-08f;  // x 2^-24
+    if (LUTB) {
+#pragma unroll
+      for (int w = 0; w < 16; ++w) lut_x_pairs(xr + 4 * w);  // (c, c+2) pairing of the table lookups
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < 64; ++i) xr[i] = 0u;
@@ -213,19 +300,45 @@ __device__ __forceinline__ void gemv_cta(const GemvParams& p, uint8_t* smem, int
     const int nr = min(TRS, r1 - ra);
     float part[kGemvMaxRPS] = {0.f, 0.f, 0.f, 0.f};
     if (warp_active) {
+      if (PAIR && !LUTB) {
 #pragma unroll 1
-      for (int m = 0; m < RPS; ++m) {
-        const int rr = (m * nteam + team) * M + rsub;  // row within the stage
-        float v = 0.f;
-        if (active && rr < nr) {
-          const float s24 = __half2float(__ushort_as_half(ss[rr * G + g])) * 16777216.f;  // s * 2^24
-          const float z = (float)sz[rr * G + g];
-          v = row_group_dot<BITS>(sw + (size_t)rr * p.row_bytes + g * GB, xr, Xs, s24, z, rot);
+        for (int m = 0; m < RPS; m += 2) {
+          const int rr0 = (m * nteam + team) * M + rsub, rr1 = ((m + 1) * nteam + team) * M + rsub;
+          const bool ok0 = active && rr0 < nr, ok1 = active && m + 1 < RPS && rr1 < nr;
+          float v0 = 0.f, v1 = 0.f;
+          if (ok0) {
+            const int q1 = ok1 ? rr1 : rr0;
+            const float s0 = __half2float(__ushort_as_half(ss[rr0 * G + g])) * 16777216.f;  // s * 2^24
+            const float s1 = __half2float(__ushort_as_half(ss[q1 * G + g])) * 16777216.f;
+            row_group_dot2<BITS>(sw + (size_t)rr0 * p.row_bytes + g * GB, sw + (size_t)q1 * p.row_bytes + g * GB, xr, Xs,
+                                 s0, (float)sz[rr0 * G + g], s1, (float)sz[q1 * G + g], rot, v0, v1);
+            if (!ok1) v1 = 0.f;
+          }
+          part[0] = m == 0 ? v0 : part[0];
+          part[1] = m == 0 ? v1 : part[1];
+          part[2] = m == 2 ? v0 : part[2];
+          part[3] = m == 2 ? v1 : part[3];
         }
-        part[0] = m == 0 ? v : part[0];
-        part[1] = m == 1 ? v : part[1];
-        part[2] = m == 2 ? v : part[2];
-        part[3] = m == 3 ? v : part[3];
+      } else {
+#pragma unroll 1
+        for (int m = 0; m < RPS; ++m) {
+          const int rr = (m * nteam + team) * M + rsub;  // row within the stage
+          float v = 0.f;
+          if (active && rr < nr) {
+            if (LUTB) {
+              v = row_group_dot_lut<LUTB ? LUTB : 3>(sw + (size_t)rr * p.row_bytes + g * GB,
+                                                      reinterpret_cast<const uint32_t*>(sw + p.off_s + (size_t)rr * p.s_row), xr, rot);
+            } else {
+              const float s24 = __half2float(__ushort_as_half(ss[rr * G + g])) * 16777216.f;  // s * 2^24
+              const float z = (float)sz[rr * G + g];
+              v = row_group_dot<BITS>(sw + (size_t)rr * p.row_bytes + g * GB, xr, Xs, s24, z, rot);
+            }
+          }
+          part[0] = m == 0 ? v : part[0];
+          part[1] = m == 1 ? v : part[1];
+          part[2] = m == 2 ? v : part[2];
+          part[3] = m == 3 ? v : part[3];
+        }
       }
     }
     __syncwarp();
@@ -304,7 +417,7 @@ __device__ __forceinline__ void gemv_cta(const GemvParams& p, uint8_t* smem, int
   if (ct == 0) DECDEC_GTRACE(p, 4);
 }
 
-template <int BITS>
+template <int BITS, int PAIR, int LUTB>
 __device__ __forceinline__ void gemv_kernel_body(const GemvParams& p) {
   extern __shared__ __align__(128) uint8_t smem[];
   // the next layer's CTAs may become resident now (two CTAs per SM): they fill their weight
@@ -316,18 +429,16 @@ __device__ __forceinline__ void gemv_kernel_body(const GemvParams& p) {
     const int i = (int)threadIdx.x * 8 + ((int)blockIdx.x & 7);
     if (i < lines) prefetch_l2(reinterpret_cast<const uint8_t*>(p.x) + ((size_t)i << 7));
   }
-  gemv_cta<BITS>(p, smem, (int)blockIdx.x - p.cta0);
+  gemv_cta<BITS, PAIR, LUTB>(p, smem, (int)blockIdx.x - p.cta0);
 }
 
-// 8 consumer warps, <= 112 registers: two CTAs per SM (the next layer's CTA co-resident)
-template <int BITS>
-__global__ void __maxnreg__(112) k_gemv(const GemvParams p) {
-  gemv_kernel_body<BITS>(p);
-}
-// 16 consumer warps, one CTA per SM
-template <int BITS>
-__global__ void __maxnreg__(120) k_gemv16(const GemvParams p) {
-  gemv_kernel_body<BITS>(p);
+// 1 producer + 15 consumer warps, one CTA per SM.  (Measured: a two-CTAs-per-SM variant with
+// 8 warps each -- the next layer's CTA resident and its ring filled before this layer ends --
+// did co-reside, but 8 warps computing cost more than the overlap won: k_chunk-0 step 1.44 vs
+// 1.25 ms.)
+template <int BITS, int PAIR, int LUTB = 0>
+__global__ void __launch_bounds__(512, 1) k_gemv16(const GemvParams p) {
+  gemv_kernel_body<BITS, PAIR, LUTB>(p);
 }
 
 }  // namespace decdec

@@ -527,7 +527,10 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
   for (int m = 0; m < MAXC; ++m) v[m] = m < nv ? __ldg(x4 + m) : make_uint4(0, 0, 0, 0);
   SEL_TRACE(16);
   uint4* sx = reinterpret_cast<uint4*>(SS + 1);  // staged keys for the finisher warp
-  // ---- coarse histogram (key >> 7), 4 copies
+  // ---- coarse histogram (key >> 7), 4 copies.  (Measured: a pre-filter that counts only keys
+  // at or above the bin of the q-th largest per-thread maximum cut the atomics ~10x but its
+  // extra barrier + bin search made the coarse phase ~1100 cycles SLOWER at 4096 and 14336 keys:
+  // the atomics are not what bounds this phase.)
   uint32_t* hA = S->histA[lane & (kHistACopies - 1)];
 #pragma unroll
   for (int m = 0; m < MAXC; ++m) {

@@ -77,6 +77,8 @@ class QuantLinear:
     def __init__(self):
         self.host = None
         self.host_scales_off = 0
+        self.w_format = 0  # DECDEC_WFMT_UNIFORM
+        self.lut = None
 
     @classmethod
     def from_codes(cls, q, s, z, bits, rc=None, rS=None, r16=None, device="cuda", numa_node=-1,
@@ -109,6 +111,34 @@ class QuantLinear:
         return self
 
     @classmethod
+    def from_lut_codes(cls, q, lut, bits, device="cuda"):
+        """Non-uniform (LUT) base layer (NEXT-3): q uint8 [d_in, d_out] codes < 2^bits, lut fp16
+        [2^bits, d_out] (oracle layout).  Codes are packed as W4K nibbles by the C++ packer; the
+        device table is [d_out][2^bits]."""
+        self = cls()
+        q = np.asarray(q)
+        d_in, d_out = q.shape
+        self.d_in, self.d_out, self.bits = d_in, d_out, bits
+        self.w = torch.from_numpy(pack_weights(q, 4).view(np.uint8).reshape(-1)).to(device)
+        self.lut = torch.from_numpy(np.ascontiguousarray(np.asarray(lut, np.float16).T).reshape(-1)).to(device)
+        self.s = self.z = None
+        self.r_bits = 0
+        self.w_format = 1
+        self._L = self._struct()
+        return self
+
+    @classmethod
+    def from_device_lut(cls, d_in, d_out, bits, w, lut):
+        """Wrap device tensors of a LUT layer (perf harness): w uint8 W4K nibbles [d_out*d_in/2],
+        lut fp16 [d_out * 2^bits]."""
+        self = cls()
+        self.d_in, self.d_out, self.bits = d_in, d_out, bits
+        self.w, self.lut, self.s, self.z = w, lut, None, None
+        self.r_bits, self.w_format = 0, 1
+        self._L = self._struct()
+        return self
+
+    @classmethod
     def from_device_packed(cls, d_in, d_out, bits, w, s, z, host=None, r_bits=4, host_scales_off=0):
         """Wrap already-packed device tensors (perf harness): w uint8 [d_out*d_in*bits/8],
         s int16/fp16 [d_out*G], z uint8 [d_out*G]; host: HostBuffer with Rq rows + scales."""
@@ -122,7 +152,11 @@ class QuantLinear:
     def _struct(self) -> decdec_layer:
         L = decdec_layer()
         L.d_in, L.d_out, L.w_bits, L.group_size = self.d_in, self.d_out, self.bits, GROUP
-        L.w_packed, L.w_scales, L.w_zeros = self.w.data_ptr(), self.s.data_ptr(), self.z.data_ptr()
+        L.w_packed = self.w.data_ptr()
+        L.w_scales = self.s.data_ptr() if self.s is not None else None
+        L.w_zeros = self.z.data_ptr() if self.z is not None else None
+        L.w_format = self.w_format
+        L.w_lut = self.lut.data_ptr() if self.lut is not None else None
         L.r_bits = self.r_bits or 4
         if self.host is not None:
             L.r_rows = self.host.ptr

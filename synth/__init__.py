@@ -13,5 +13,7 @@ from .inputs import (  # noqa: F401
     gen_special_activations,
     gen_perf_layer,
     gen_perf_layer_device,
+    gen_perf_layer_lut,
+    gen_perf_layer_lut_device,
     model_layers,
 )

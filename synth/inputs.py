@@ -127,3 +127,38 @@ def gen_perf_layer_device(d_in: int, d_out: int, bits: int, seed: int, device="c
     r = lo | (hi << 4)
     rS = (s.float().view(d_out, G).median(dim=1).values / 14.0).to(torch.float16)
     return dict(w=w, s=s, z=z, r=r, rS=rS)
+
+
+def gen_perf_layer_lut(d_in: int, d_out: int, bits: int, seed: int, with_residual: bool = True):
+    """Stored quantities of one non-uniform (LUT) layer drawn directly (NEXT-3 perf / parity
+    configs; the SqueezeLLM-style base of P:397): q ~ U[0, 2^b - 1]; per column a sorted table
+    of 2^b fp16 values ~ N(0, 0.02^2) x LogNormal(0, 0.25) (a k-means table's shape); residual
+    codes ~ U[-7, 7], S_j = fp16(median gap of column j's table / 14).
+    Returns dict q uint8 [d_in, d_out], lut fp16 [2^b, d_out], rc, rS."""
+    rng = np.random.default_rng(seed)
+    n = 1 << bits
+    q = rng.integers(0, n, size=(d_in, d_out), dtype=np.uint8)
+    col = rng.lognormal(0.0, 0.25, size=d_out)
+    lut = np.sort(rng.normal(0.0, 0.02, size=(n, d_out)) * col[None, :], axis=0).astype(np.float16)
+    out = dict(q=q, lut=lut)
+    if with_residual:
+        out["rc"] = rng.integers(-7, 8, size=(d_in, d_out), dtype=np.int8)
+        gaps = np.diff(lut.astype(np.float64), axis=0)
+        out["rS"] = (np.median(gaps, axis=0) / 14.0).astype(np.float16)
+    return out
+
+
+def gen_perf_layer_lut_device(d_in: int, d_out: int, bits: int, seed: int, device="cuda"):
+    """Perf-harness LUT layer drawn on the GPU: W4K nibble codes uniform on [0, 2^b - 1] (random
+    bytes with each nibble masked; W4K is a bijection between codes and words) and per-column
+    sorted fp16 tables [d_out][2^b] (the shape of gen_perf_layer_lut's)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed & 0x7FFFFFFFFFFFFFFF)
+    n = 1 << bits
+    mask = (n - 1) | ((n - 1) << 4)
+    w = torch.randint(0, 256, (d_out * d_in // 2,), dtype=torch.uint8, device=device, generator=g) & mask
+    col = torch.exp(torch.randn(d_out, 1, device=device, generator=g) * 0.25)
+    lut = torch.sort(torch.randn(d_out, n, device=device, generator=g) * 0.02 * col, dim=1).values.to(torch.float16)
+    return dict(w=w, lut=lut.reshape(-1))

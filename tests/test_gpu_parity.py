@@ -311,6 +311,45 @@ def test_r16_llama_o_shape():
         check_full(y, ref, f"r16/o/kc{kc}")
 
 
+# ------------------------------------------------------------------ NEXT-3: non-uniform (LUT) base
+@pytest.mark.parametrize("bits", [3, 4])
+def test_lut_config1_full_pipeline(bits):
+    """SqueezeLLM-style LUT base (ledger L17): seeded fp16 W -> oracle k-means
+    tables -> the LUT GEMV kernel, every output column within L9; codes decoded bit-exact."""
+    d_in, d_out = SHAPES["config1"]["l"]
+    W = gen_weight_fp16(d_in, d_out, layer_seed("lut", "W", bits))
+    q, lut = oracle.quantize_base_lut(W, bits)
+    lin = dd.QuantLinear.from_lut_codes(q, lut, bits)
+    assert np.array_equal(lin.debug_unpack().cpu().numpy(), q.T)
+    plan = _plan(lin, 0)
+    assert plan["kernel"] == "k_gemv"
+    X = gen_activations(d_in, 4, seed=layer_seed("lut", "x", bits))
+    for xi, x in enumerate(X):
+        y = lin(to_dev(x), 0)
+        ref = decdec_linear_ref(q, None, None, x, 0, lut=lut)
+        check_full(y, ref, f"lut/config1/b{bits}/x{xi}")
+        assert torch.equal(y, lin.gemv(to_dev(x)))
+    with pytest.raises(dd.DecdecError) as e:   # compensation on LUT layers: not built (header)
+        lin(to_dev(X[0]), 16, workspace=dd.Workspace(16, d_out))
+    assert e.value.status == -4
+
+
+@pytest.mark.parametrize("bits", [3, 4])
+@pytest.mark.parametrize("model,name", [("llama3_8b", "qkv"), ("llama3_8b", "o"), ("llama3_8b", "gu"),
+                                        ("llama3_8b", "d"), ("phi3_medium", "o"), ("phi3_medium", "d")])
+def test_lut_shapes_all_columns(bits, model, name):
+    from synth import gen_perf_layer_lut
+
+    d_in, d_out = SHAPES[model][name]
+    L = gen_perf_layer_lut(d_in, d_out, bits, seed=layer_seed("lutperf", model, name, bits), with_residual=False)
+    lin = dd.QuantLinear.from_lut_codes(L["q"], L["lut"], bits)
+    W_hat = oracle.dequantize_lut(L["q"], L["lut"])
+    x = gen_activations(d_in, 1, seed=layer_seed("lutperf", name, "x"), kind="d" if name == "d" else "qkv")[0]
+    y = lin(to_dev(x), 0)
+    ref = decdec_linear_ref(L["q"], None, None, x, 0, W_hat=W_hat)
+    check_full(y, ref, f"lut/{model}/{name}/b{bits}")
+
+
 @pytest.mark.parametrize("kind", ["all_equal", "zeros", "ties", "sparse"])
 def test_fused_selection_ties_and_degenerate(kind):
     """The fused layer kernel's own (split-order) selector on tie-heavy / degenerate x: the
@@ -534,3 +573,18 @@ def test_validation_error_codes():
     with pytest.raises(dd.DecdecError) as e:
         dd.decdec_debug_selections(idx.data_ptr(), xs.data_ptr(), 0, 4)
     assert e.value.status == -1
+
+
+def test_concurrent_streams_no_deadlock():
+    """Liveness (include/decdec.h "one workspace per concurrent stream"): three streams issue
+    compensated calls back to back; the fused grids are launched cooperatively, so none is ever
+    left partially resident while its DEC CTAs wait.  Run in a child process with a timeout so a
+    hang fails the test instead of the session."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "concurrency_check.py"), "--iters", "40"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert '"bit_identical_to_serial": true' in r.stdout
