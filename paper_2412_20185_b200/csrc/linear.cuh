@@ -266,6 +266,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   // ---- steps 2-3: gather rows S of R_hat x x[S] for this CTA's segments (double-buffered)
   if (it < n_items && !issued) {
     ready(it);
+    if (tr && warp == 0 && lane == 0) tr[2] = clock64();  // DEC CTAs: cycle stamps in slots 2-4, 10
     issue(it, 0);
   }
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -279,6 +280,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     } else {
       cp_async_wait<0>();
     }
+    if (tr && warp == 0 && lane == 0 && it == 0) tr[3] = clock64();  // first item landed
     consume(it, b, acc);
     if (!one_seg) store_part(it % ns, it / ns, acc);
   }
@@ -296,6 +298,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   }
   __syncthreads();  // all partials of the CTA's segments are in smem
   if (RBITS == 4 && warp < ns) mbar_wait(scale_bar, 0);  // the scales' bulk copies landed
+  if (tr && threadIdx.x == 0) tr[4] = clock64();
   if (threadIdx.x == 0) DECDEC_TRACE(p, 12);
   // ---- step 4: combine, one warp per local segment.  o_b entries are self-validating (relaxed
   // stores of the GEMV CTAs, kObEmpty until written): poll them, then restore kObEmpty.
@@ -314,6 +317,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
         o0 = ld_relaxed_gpu_u4(p.ob + col0);
         o1 = ld_relaxed_gpu_u4(p.ob + col0 + 4);
       }
+      if (tr && i == 0 && lane == 0) tr[10] = clock64();  // o_b rows seen
       float sum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       for (int j = 0; j < p.nparts; ++j) {  // fixed order: slots ascending
         const float* pp = spart + ((size_t)i * p.nparts + j) * kSegCols + lane * 8;

@@ -7,7 +7,7 @@ cat /sys/kernel/mm/transparent_hugepage/enabled /sys/kernel/mm/transparent_hugep
 B="python bench.py --steps ${STEPS:-30} --warmup 5 --sweep ${SWEEP:-0,1,21} --no-cpu-baseline --no-w4 --no-unfused-extra --no-lut --sweep-only ${BARGS:-}"
 for rep in 1 2; do
 for s in "$@"; do
-  env $s timeout 600 $B > gpurun_out/${T}_$(echo $s | tr '=, ' '___')_$rep.json 2>gpurun_out/${T}_err.txt || tail -5 gpurun_out/${T}_err.txt
+  env $s timeout 600 $B > gpurun_out/${T}_$(echo $s | tr '=, /.' '_____')_$rep.json 2>gpurun_out/${T}_err.txt || tail -5 gpurun_out/${T}_err.txt
 done
 done
 python - "$T" <<'PY'

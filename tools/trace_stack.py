@@ -106,8 +106,9 @@ for i, (b, name, d_in, d_out) in enumerate(meta):
     dec = ev[(ev[:, 5] > 0) & (ev[:, 8] == 0)]
     if len(dec):
         d0 = dec[0]
-        rows.append((f"{b}:{name}", [d0[j] - d0[15] for j in (16, 17, 18, 11, 13, 19, 14)]))
+        rows.append((f"{b}:{name}", [d0[j] - d0[15] for j in (16, 17, 18, 11, 13, 19, 14, 2, 3, 4, 10)]))
 if rows:
-    print("DEC CTA 0 selection phases (SM cycles after sel_start): loads issued, coarse bin, D placed, finisher: T found, R placed, published; warp 0 done")
-    for n, r in rows[:8]:
+    print("DEC CTA 0 phases (SM cycles after sel_start): loads issued, coarse bin, D placed, finisher: T found, R placed, "
+          "published; warp 0 done, warp 0 first issue, first item landed, scales landed (combine), o_b seen")
+    for n, r in rows[:12]:
         print(f"  {n:8s}", " ".join(f"{v:7.0f}" for v in r))
