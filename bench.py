@@ -244,11 +244,15 @@ def time_shapes(torch, dist, dd, M, ws, sweep, steps, stream, world, bits, hbm_p
     return per_shape
 
 
-def step_sweep(torch, dist, dd, M, ws, sweep, steps, warmup, stream, world, comm=None):
-    """tokens/s of the whole decode step (all layers, one CUDA graph per activation set) per k_chunk."""
+def step_sweep(torch, dist, dd, M, ws, sweep, steps, warmup, stream, world, comm=None, peers=None):
+    """tokens/s of the whole decode step (all layers, one CUDA graph per activation set) per k_chunk.
+    TP: peers -> fused P2P-store all-gather in every layer kernel (P2PStack); comm -> NCCL."""
     out = {}
     for kc in sweep:
-        if comm is None:
+        if peers is not None:
+            offs, _ = dd.peer_offsets([m[3] for m in M.meta], world)
+            stacks = [dd.P2PStack(M.layers, M.ks(kc), M.xs(s), offs, ws, peers) for s in range(len(M.x_dev))]
+        elif comm is None:
             stacks = [dd.Stack(M.layers, M.ks(kc), M.xs(s), M.ys(), ws) for s in range(len(M.x_dev))]
         else:
             full = [torch.empty(m[3] * world, dtype=torch.float16, device="cuda") for m in M.meta]
@@ -369,6 +373,8 @@ def main():
     ap.add_argument("--nx", type=int, default=4, help="distinct activation sets cycled across steps")
     ap.add_argument("--quick", action="store_true", help="headline step only (for ncu launch lists)")
     ap.add_argument("--sweep-only", action="store_true", help="decode-step sweep only (no per-shape table, no oracle)")
+    ap.add_argument("--tp-comm", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: assemble y with the fused P2P-store all-gather (default) or NCCL")
     ap.add_argument("--shard-of", type=int, default=1,
                     help="single GPU: run rank 0's output-feature shard of a P-way TP model (d_out/P per layer, "
                          "its own host residual slice); per-rank time, all-gather NOT included (config 4/5 evidence)")
@@ -394,9 +400,18 @@ def main():
 
     import paper_2412_20185_b200 as dd
 
+    # DECDEC_BENCH_SHARE_GPU=1 (tests only): every rank on GPU 0 over gloo -- exercises the N > 1
+    # code path (fused P2P all-gather between processes) on a one-GPU box; its timings are not
+    # bench numbers (the driver time-slices the ranks' kernels)
+    share = os.environ.get("DECDEC_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = "cuda"
     stream = torch.cuda.current_stream()
     hbm_peak, hbm_src, pcie_peak, pcie_src = load_peaks()
@@ -415,11 +430,33 @@ def main():
     torch.cuda.synchronize()
     t_build = time.time() - t_build
     n_layers = len(M.meta)
-    comm = dd.Comm() if world > 1 else None  # library-owned NCCL communicator (TP all-gather)
+    comm = peers = None
+    tp_comm = None
+    if world > 1:
+        # the y assembly: fused P2P-store all-gather in the layer kernels (default), or the
+        # library-owned NCCL communicator's all-gather after each layer kernel
+        if args.tp_comm == "p2p":
+            err = ""
+            try:
+                peers = dd.Peers(dd.peer_offsets([m[3] for m in M.meta], world)[1])
+            except Exception as e:  # no peer access between the GPUs: NCCL instead, said so in the line
+                peers, err = None, str(e)[:80]
+            ok = torch.tensor([1 if peers is not None else 0], device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
+            if int(ok.item()) == 0:
+                if peers is not None:
+                    peers.close()
+                peers = None
+                tp_comm = f"nccl (p2p unavailable: {err or 'on another rank'})"
+            else:
+                tp_comm = "p2p (fused all-gather in the layer kernels, CUDA-IPC peer stores over NVLink)"
+        if peers is None:
+            comm = dd.Comm()
+            tp_comm = tp_comm or "nccl (in-place all-gather after each layer kernel)"
 
     # ---- full decode-step graphs per k_chunk (clocks sampled over all timed regions) ---------
     sampler = ClockSampler(local) if rank == 0 else None
-    results = step_sweep(torch, dist, dd, M, ws, sweep, args.steps, args.warmup, stream, world, comm)
+    results = step_sweep(torch, dist, dd, M, ws, sweep, args.steps, args.warmup, stream, world, comm, peers)
     clocks = sampler.stop() if sampler is not None else None
     headline = (results[args.kchunk]["ms_per_step"], results[args.kchunk]["kernels_per_step"])
 
@@ -579,7 +616,7 @@ def main():
                                    f"{M.n_blocks} blocks, w{args.bits} g128, r4 residual in pinned host memory, "
                                    f"exact Top-k, k_chunk={args.kchunk}",
                        "k_chunk": args.kchunk, "layers_per_step": n_layers,
-                       "parallelism": (f"tp{world} (output-feature shards + NCCL all-gather)" if world > 1 else
+                       "parallelism": (f"tp{world} (output-feature shards; y assembly: {tp_comm})" if world > 1 else
                                        f"single GPU running rank 0's 1/{shard} output-feature shard (all-gather not included)"
                                        if shard > 1 else "single GPU"),
                        "l2": f"inputs larger than L2: {step_hbm / 1e9:.2f} GB weights streamed per step",

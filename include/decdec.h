@@ -195,6 +195,49 @@ decdec_status decdec_stack_create_tp(const decdec_layer* layers, int32_t n_layer
                                      const uint16_t* const* x, uint16_t* const* y_full, void* ws, size_t ws_bytes,
                                      decdec_comm* comm, decdec_stream_t stream, decdec_stack** out);
 
+/* ---- fused P2P-store all-gather (the exchange inside the layer
+ * kernel's epilogue instead of a separate collective).  Each rank owns a symmetric device
+ * region: a flag area (1024 per-layer completion counters) and a user area of user_bytes
+ * holding the y_full buffers, at the same offsets on every rank.  The layer kernel stores its
+ * shard's fp16 outputs into EVERY rank's y_full through CUDA-IPC peer mappings (NVLink stores
+ * on a multi-GPU node), releases one count per writing CTA to every rank's flag of the layer's
+ * slot, and completes only after this rank's flag shows all nranks' shards (acquire, system
+ * scope).  The launch is cooperative (every CTA co-resident), so the wait cannot starve the
+ * writers.  Ranks may share one GPU (separate processes; the driver time-slices them). */
+typedef struct decdec_peers decdec_peers;
+#define DECDEC_IPC_HANDLE_BYTES 64
+
+/* This rank's region on the current device (zeroed); handle_out (64 bytes, host) receives its
+ * IPC handle, to be exchanged with the other ranks out of band (e.g. the torch process group).
+ * Errors: DECDEC_EINVAL (NULL args), DECDEC_ECUDA (allocation / IPC export failed). */
+decdec_status decdec_peers_create(size_t user_bytes, void* handle_out, decdec_peers** out);
+/* Open every other rank's region; handles = nranks x 64 bytes in rank order (this rank's own
+ * entry is ignored).  1 <= nranks <= 8, once per group.  DECDEC_ECUDA if a handle cannot be
+ * opened (no peer access between the devices). */
+decdec_status decdec_peers_connect(decdec_peers* p, int32_t rank, int32_t nranks, const void* handles);
+/* Device address / size of this rank's user area (NULL / 0 if p is NULL). */
+void* decdec_peers_buffer(const decdec_peers* p);
+size_t decdec_peers_buffer_bytes(const decdec_peers* p);
+void decdec_peers_destroy(decdec_peers* p);
+
+/* decdec_linear on this rank's shard L (d_out_r = L->d_out) whose outputs land at byte offset
+ * y_off of EVERY rank's user area: y_full = buffer + y_off, fp16 [nranks*d_out_r], this rank's
+ * shard at y_full + rank*d_out_r.  On return (stream order) y_full is complete on this rank.
+ * slot (0..1023) names the completion counter; calls that may overlap in time across ranks
+ * (consecutive layers) need distinct slots, and every rank must issue the same sequence of
+ * (slot, shape, k, chunk).  y_off must be 16-B aligned and y_off + nranks*d_out_r*2 <= user
+ * bytes.  sel/ws as decdec_linear.  Errors as decdec_linear; DECDEC_EINVAL if the peer group is
+ * not connected or slot/y_off are out of range; DECDEC_EUNSUPPORTED for LUT-base layers. */
+decdec_status decdec_linear_p2p(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk, size_t y_off,
+                                int32_t slot, int32_t* sel, void* ws, size_t ws_bytes, decdec_peers* peers,
+                                decdec_stream_t stream);
+
+/* A TP decode step with the fused all-gather, captured as one CUDA graph: layer i as
+ * decdec_linear_p2p(layers[i], x[i], k[i], chunk, y_off[i], slot = i) (n_layers <= 1024). */
+decdec_status decdec_stack_create_p2p(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
+                                      const uint16_t* const* x, const size_t* y_off, void* ws, size_t ws_bytes,
+                                      decdec_peers* peers, decdec_stream_t stream, decdec_stack** out);
+
 /* ------------------------------------------------------------------ offline, host-only */
 /* Pack base codes q (u8 [d_in][d_out], logical W layout, values < 2^bits) into W3K/W4K
  * (uint32 [d_out][d_in*bits/32]).  out_bytes must be >= d_out*d_in*bits/8. */

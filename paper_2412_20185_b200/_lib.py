@@ -73,6 +73,13 @@ def _load():
         "decdec_comm_nranks": (I32, [VP]),
         "decdec_linear_tp": (I32, [Lp, VP, I32, I32, VP, VP, VP, SZ, VP, VP]),
         "decdec_stack_create_tp": (I32, [Lp, I32, P(I32), I32, P(VP), P(VP), VP, SZ, VP, VP, P(VP)]),
+        "decdec_peers_create": (I32, [SZ, VP, P(VP)]),
+        "decdec_peers_connect": (I32, [VP, I32, I32, VP]),
+        "decdec_peers_buffer": (VP, [VP]),
+        "decdec_peers_buffer_bytes": (SZ, [VP]),
+        "decdec_peers_destroy": (None, [VP]),
+        "decdec_linear_p2p": (I32, [Lp, VP, I32, I32, SZ, I32, VP, VP, SZ, VP, VP]),
+        "decdec_stack_create_p2p": (I32, [Lp, I32, P(I32), I32, P(VP), P(SZ), VP, SZ, VP, VP, P(VP)]),
     }
     for name, (res, args) in sig.items():
         if os.environ.get("DECDEC_LIB") and not hasattr(lib, name):
@@ -92,6 +99,8 @@ EXPORTED = [
     "decdec_stack_kernels", "decdec_stack_destroy", "decdec_debug_trace", "decdec_debug_selections",
     "decdec_set_dec_ctas", "decdec_nccl_version", "decdec_nccl_unique_id", "decdec_comm_init", "decdec_comm_destroy",
     "decdec_comm_rank", "decdec_comm_nranks", "decdec_linear_tp", "decdec_stack_create_tp",
+    "decdec_peers_create", "decdec_peers_connect", "decdec_peers_buffer", "decdec_peers_buffer_bytes",
+    "decdec_peers_destroy", "decdec_linear_p2p", "decdec_stack_create_p2p",
 ]
 
 
@@ -262,4 +271,53 @@ def decdec_stack_create_tp(layers, ks, chunk, xs, ys_full, ws, ws_bytes, comm, s
     out = ctypes.c_void_p()
     _check(_lib.decdec_stack_create_tp(arr, n, karr, chunk, xarr, yarr, _vp(ws), ws_bytes, _vp(comm), _vp(stream),
                                        ctypes.byref(out)), "decdec_stack_create_tp")
+    return int(out.value)
+
+
+# ---- fused P2P-store all-gather (decdec_peers)
+IPC_HANDLE_BYTES = 64
+
+
+def decdec_peers_create(user_bytes: int):
+    """-> (peers handle, 64-byte IPC handle of this rank's region)"""
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    out = ctypes.c_void_p()
+    _check(_lib.decdec_peers_create(user_bytes, h, ctypes.byref(out)), "decdec_peers_create")
+    return int(out.value), h.raw
+
+
+def decdec_peers_connect(p, rank: int, nranks: int, handles: bytes):
+    if len(handles) != nranks * IPC_HANDLE_BYTES:
+        raise ValueError("handles must be nranks x 64 bytes")
+    buf = ctypes.create_string_buffer(handles, len(handles))
+    _check(_lib.decdec_peers_connect(_vp(p), rank, nranks, buf), "decdec_peers_connect")
+
+
+def decdec_peers_buffer(p) -> int:
+    return int(_lib.decdec_peers_buffer(_vp(p)) or 0)
+
+
+def decdec_peers_buffer_bytes(p) -> int:
+    return int(_lib.decdec_peers_buffer_bytes(_vp(p)))
+
+
+def decdec_peers_destroy(p):
+    _lib.decdec_peers_destroy(_vp(p))
+
+
+def decdec_linear_p2p(L: decdec_layer, x, k: int, chunk: int, y_off: int, slot: int, sel, ws, ws_bytes: int, peers,
+                      stream=0):
+    _check(_lib.decdec_linear_p2p(ctypes.byref(L), _vp(x), k, chunk, y_off, slot, _vp(sel), _vp(ws), ws_bytes,
+                                  _vp(peers), _vp(stream)), "decdec_linear_p2p")
+
+
+def decdec_stack_create_p2p(layers, ks, chunk, xs, y_offs, ws, ws_bytes, peers, stream=0) -> int:
+    n = len(layers)
+    arr = (decdec_layer * n)(*layers)
+    karr = (ctypes.c_int32 * n)(*[int(k) for k in ks])
+    xarr = (ctypes.c_void_p * n)(*[int(p) for p in xs])
+    oarr = (ctypes.c_size_t * n)(*[int(o) for o in y_offs])
+    out = ctypes.c_void_p()
+    _check(_lib.decdec_stack_create_p2p(arr, n, karr, chunk, xarr, oarr, _vp(ws), ws_bytes, _vp(peers), _vp(stream),
+                                        ctypes.byref(out)), "decdec_stack_create_p2p")
     return int(out.value)

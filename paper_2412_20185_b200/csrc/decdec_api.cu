@@ -10,6 +10,7 @@
 #include "gemv.cuh"
 #include "linear.cuh"
 #include "select.cuh"
+#include "p2p_internal.h"
 #include "tp_internal.h"
 
 using namespace decdec;
@@ -465,7 +466,9 @@ decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, c
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  if (p.k_sel > 0 && coop_launch()) {
+  // cooperative: DEC CTAs wait for GEMV CTAs of the same grid; the fused P2P all-gather's
+  // leader waits for the other CTAs' signals
+  if ((p.k_sel > 0 && coop_launch()) || p.pp.nranks > 1) {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na].val.cooperative = 1;
     ++na;
@@ -727,6 +730,34 @@ decdec_status enqueue_linear(const Prepared& P, cudaStream_t st, bool chained = 
   return launch_linear(P.p, pl, P.bits, P.p.k_sel ? P.rbits : 4, chained, st);
 }
 
+// This rank's shard pointer inside the user area of its peer region (decdec_linear_p2p).
+uint16_t* p2p_shard(const decdec_peers* pe, int q, size_t y_off, int d_out) {
+  return reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(pe->base[q]) + decdec::kFlagBytes + y_off) +
+         (size_t)pe->rank * d_out;
+}
+
+decdec_status check_p2p(const decdec_layer* L, const decdec_peers* pe, size_t y_off, int slot) {
+  if (!L || !pe || pe->nranks < 1) return DECDEC_EINVAL;
+  if (slot < 0 || slot >= decdec::kFlagSlots || (y_off & 15)) return DECDEC_EINVAL;
+  if (y_off + (size_t)pe->nranks * L->d_out * 2 > pe->user_bytes) return DECDEC_ESPACE;
+  return DECDEC_OK;
+}
+
+// Fused all-gather parameters of a prepared layer call (p2p.cuh).
+decdec_status fill_p2p(Prepared* P, const decdec_layer* L, const decdec_peers* pe, size_t y_off, int slot) {
+  if (P->gemv) return DECDEC_EUNSUPPORTED;  // LUT base / DECDEC_NEW_GEMV: k_gemv16 has no exchange epilogue
+  decdec::P2PParams& pp = P->p.pp;
+  pp.nranks = pe->nranks;
+  pp.n_writers = P->p.k_sel > 0 ? P->pl.n_dec : P->pl.grid;  // DEC CTAs (combine) or GEMV CTAs write y
+  pp.leader = 0;
+  for (int q = 0; q < pe->nranks; ++q) {
+    pp.peer_y[q] = p2p_shard(pe, q, y_off, L->d_out);
+    pp.peer_flag[q] = static_cast<unsigned int*>(pe->base[q]) + (size_t)slot * decdec::kFlagStrideWords;
+  }
+  pp.my_flag = pp.peer_flag[pe->rank];
+  return DECDEC_OK;
+}
+
 }  // namespace
 
 struct decdec_stack {
@@ -753,8 +784,10 @@ namespace {
 // followed by the in-place all-gather of y[i].
 decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
                            const uint16_t* const* x, uint16_t* const* y, void* ws, size_t ws_bytes,
-                           decdec_comm* comm, decdec_stack** out) {
-  if (!layers || n_layers <= 0 || !k || !x || !y || !out) return DECDEC_EINVAL;
+                           decdec_comm* comm, decdec_stack** out, decdec_peers* peers = nullptr,
+                           const size_t* y_off = nullptr) {
+  if (!layers || n_layers <= 0 || !k || !x || !out) return DECDEC_EINVAL;
+  if (peers ? (!y_off || n_layers > decdec::kFlagSlots || peers->nranks < 1) : !y) return DECDEC_EINVAL;
   *out = nullptr;
   if (g_trace && g_trace_bytes < (2 + (size_t)n_layers * kTraceStride) * 8) return DECDEC_ESPACE;
   const int rank = comm ? tp_rank(comm) : 0;
@@ -763,8 +796,16 @@ decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const i
   decdec_status s = DECDEC_OK;
   int n_kernels = 0;
   for (int i = 0; i < n_layers && s == DECDEC_OK; ++i) {
-    uint16_t* yi = y[i] ? y[i] + (size_t)rank * layers[i].d_out : nullptr;
-    s = prepare_linear(&layers[i], x[i], k[i], chunk, yi, nullptr, ws, ws_bytes, &P[i]);
+    if (peers) {  // fused all-gather: layer i writes every rank's y_full at y_off[i], slot i
+      s = check_p2p(&layers[i], peers, y_off[i], i);
+      if (s == DECDEC_OK)
+        s = prepare_linear(&layers[i], x[i], k[i], chunk, p2p_shard(peers, peers->rank, y_off[i], layers[i].d_out),
+                           nullptr, ws, ws_bytes, &P[i]);
+      if (s == DECDEC_OK) s = fill_p2p(&P[i], &layers[i], peers, y_off[i], i);
+    } else {
+      uint16_t* yi = y[i] ? y[i] + (size_t)rank * layers[i].d_out : nullptr;
+      s = prepare_linear(&layers[i], x[i], k[i], chunk, yi, nullptr, ws, ws_bytes, &P[i]);
+    }
     // debug timelines: one trace region per layer (decdec_debug_trace buffer must hold them)
     if (g_trace) {
       P[i].p.trace = g_trace + 2 + (size_t)i * kTraceStride;
@@ -850,6 +891,26 @@ decdec_status decdec_stack_create_tp(const decdec_layer* layers, int32_t n_layer
   (void)stream;
   if (!comm) return DECDEC_EINVAL;
   return stack_create(layers, n_layers, k, chunk, x, y_full, ws, ws_bytes, comm, out);
+}
+
+decdec_status decdec_stack_create_p2p(const decdec_layer* layers, int32_t n_layers, const int32_t* k, int32_t chunk,
+                                      const uint16_t* const* x, const size_t* y_off, void* ws, size_t ws_bytes,
+                                      decdec_peers* peers, decdec_stream_t stream, decdec_stack** out) {
+  (void)stream;
+  if (!peers) return DECDEC_EINVAL;
+  return stack_create(layers, n_layers, k, chunk, x, nullptr, ws, ws_bytes, nullptr, out, peers, y_off);
+}
+
+decdec_status decdec_linear_p2p(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk, size_t y_off,
+                                int32_t slot, int32_t* sel, void* ws, size_t ws_bytes, decdec_peers* peers,
+                                decdec_stream_t stream) {
+  decdec_status s = check_p2p(L, peers, y_off, slot);
+  if (s != DECDEC_OK) return s;
+  Prepared P;
+  s = prepare_linear(L, x, k, chunk, p2p_shard(peers, peers->rank, y_off, L->d_out), sel, ws, ws_bytes, &P);
+  if (s != DECDEC_OK) return s;
+  if ((s = fill_p2p(&P, L, peers, y_off, slot)) != DECDEC_OK) return s;
+  return enqueue_linear(P, (cudaStream_t)stream);
 }
 
 decdec_status decdec_stack_launch(decdec_stack* g, decdec_stream_t stream) {

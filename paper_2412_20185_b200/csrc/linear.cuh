@@ -29,6 +29,7 @@
 #include <type_traits>
 #include "ptx.cuh"
 #include "decode.cuh"
+#include "p2p.cuh"
 #include "select.cuh"
 
 namespace decdec {
@@ -95,6 +96,7 @@ struct LinearParams {
   int* dbg_idx;
   uint16_t* dbg_xs;
   int dbg_cap, dbg_ctas;
+  P2PParams pp;  // fused P2P all-gather (p2p.cuh); pp.nranks <= 1: plain local y stores
 };
 
 // A DEC CTA (steps 1-4 of P:207).  DEC CTA c owns the output segments c, c + n_dec, ...:
@@ -344,13 +346,20 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
         const __half hi = __float2half_rn(fmaf(Sc[2 * e + 1], sum[2 * e + 1], o[2 * e + 1]));
         out[e] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
       }
-      *reinterpret_cast<uint4*>(p.y + col0) = make_uint4(out[0], out[1], out[2], out[3]);
+      p2p_store_u4(p.pp, p.y, col0, make_uint4(out[0], out[1], out[2], out[3]));
       const uint4 empty = make_uint4(kObEmpty, kObEmpty, kObEmpty, kObEmpty);
       *reinterpret_cast<uint4*>(p.ob + col0) = empty;  // ready for the next call
       *reinterpret_cast<uint4*>(p.ob + col0 + 4) = empty;
     }
   }
   if (threadIdx.x == 0) DECDEC_TRACE(p, 9);
+  if (p.pp.nranks > 1) {  // fused all-gather: this CTA's segments are in every rank's y_full
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      p2p_signal(p.pp);
+      if ((int)blockIdx.x == p.pp.leader) p2p_wait_all(p.pp);
+    }
+  }
   if (p.dbg_idx && (int)blockIdx.x < p.dbg_ctas) {  // every DEC CTA's own selection, for tests
     if (split && nD < p.k_sel) select_wait_rest(SS);
     int* di = p.dbg_idx + (size_t)blockIdx.x * p.dbg_cap;
@@ -627,7 +636,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
           if ((lane & 7) == 0) {  // lane 0 -> row 0, 8 -> 1, 16 -> 2, 24 -> 3
             const int m = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
             const int row = tile * TR + slot + m * NSLOTS;
-            if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
+            if (p.k_sel == 0) p2p_store_u16(p.pp, p.y, row, __half_as_ushort(__float2half_rn(v)));
             else st_relaxed_gpu_f32(p.ob + row, v);
           }
         } else if (G == 32 && RPS == 2) {
@@ -637,7 +646,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
           for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
           if ((lane & 15) == 0) {
             const int row = tile * TR + slot + (hi16 ? 1 : 0) * NSLOTS;
-            if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
+            if (p.k_sel == 0) p2p_store_u16(p.pp, p.y, row, __half_as_ushort(__float2half_rn(v)));
             else st_relaxed_gpu_f32(p.ob + row, v);
           }
         } else {
@@ -648,7 +657,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
             for (int o = G >> 1; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if (g == 0) {
               const int row = tile * TR + slot + m * NSLOTS;
-              if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
+              if (p.k_sel == 0) p2p_store_u16(p.pp, p.y, row, __half_as_ushort(__float2half_rn(v)));
               else st_relaxed_gpu_f32(p.ob + row, v);
             }
           }
@@ -671,7 +680,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
             float v = 0.f;
             for (int w = 0; w < p.NKW; ++w) v += rbuf[lane * p.NKW + w];
             const int row = tile * TR + slot + lane * NSLOTS;
-            if (p.k_sel == 0) p.y[row] = __half_as_ushort(__float2half_rn(v));
+            if (p.k_sel == 0) p2p_store_u16(p.pp, p.y, row, __half_as_ushort(__float2half_rn(v)));
             else st_relaxed_gpu_f32(p.ob + row, v);
           }
           nrows = RPS;
@@ -685,6 +694,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     }
     if (ct == 0) DECDEC_TRACE(p, 4);
     if (ct == 0) DECDEC_TRACE(p, 10);  // last o_b row stored (this warp)
+    if (p.k_sel == 0 && p.pp.nranks > 1) {  // fused all-gather (k = 0: the GEMV CTAs write y)
+      named_bar_sync(15, p.NC * 32);
+      if (ct == 0) {
+        p2p_signal(p.pp);
+        if ((int)blockIdx.x == p.pp.leader) p2p_wait_all(p.pp);
+      }
+    }
     return;
   }
 }

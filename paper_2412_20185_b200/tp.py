@@ -133,3 +133,111 @@ class TPStack:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------ fused P2P-store all-gather
+def peer_offsets(d_outs, world: int, align: int = 256):
+    """Byte offsets of the y_full buffers ([world * d_out_r] fp16 each) inside a peer user
+    area, and the total bytes: the same layout on every rank (symmetric memory)."""
+    offs, o = [], 0
+    for d in d_outs:
+        offs.append(o)
+        o += (world * int(d) * 2 + align - 1) // align * align
+    return offs, o
+
+
+class _DevView:
+    """__cuda_array_interface__ over raw device memory (a torch view of the peer user area)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str = "<f2"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False), "version": 3}
+
+
+class Peers:
+    """This rank's symmetric device region (decdec_peers_create) connected to every other rank's
+    (decdec_peers_connect); the 64-byte CUDA-IPC handles travel over the torch process group
+    (plumbing).  `view(off, n)` is a torch fp16 tensor over the local user area."""
+
+    def __init__(self, user_bytes: int, group=None):
+        import torch.distributed as dist
+        from paper_2412_20185_b200 import _lib
+
+        self._lib = _lib
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.handle, h = _lib.decdec_peers_create(user_bytes)
+        hs = [None] * self.world
+        dist.all_gather_object(hs, h, group=group)
+        _lib.decdec_peers_connect(self.handle, self.rank, self.world, b"".join(hs))
+        self.base = _lib.decdec_peers_buffer(self.handle)
+        self.nbytes = _lib.decdec_peers_buffer_bytes(self.handle)
+
+    def view(self, off: int, n: int):
+        import torch
+
+        if off + 2 * n > self.nbytes:
+            raise ValueError("view outside the peer user area")
+        return torch.as_tensor(_DevView(self.base + off, n), device="cuda")
+
+    def close(self):
+        if self.handle:
+            self._lib.decdec_peers_destroy(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class P2PLinear:
+    """This rank's shard of a DecDEC layer with the fused all-gather: one decdec_linear_p2p call
+    writes the shard into every rank's y_full (peer user area at byte offset y_off) and returns
+    when this rank's y_full is complete.  `slot` must differ between layers that may overlap."""
+
+    def __init__(self, shard_linear, peers: Peers, y_off: int, slot: int):
+        self.lin, self.peers, self.y_off, self.slot = shard_linear, peers, int(y_off), int(slot)
+        self.d_out_shard = shard_linear.d_out
+        self.y_full = peers.view(self.y_off, self.d_out_shard * peers.world)
+
+    def __call__(self, x, k: int, chunk: int = 0, sel=None, workspace=None, stream=None):
+        from paper_2412_20185_b200 import _lib
+        from paper_2412_20185_b200.layer import Workspace, _stream_ptr
+
+        if workspace is None:
+            workspace = Workspace(max(k, 1), self.d_out_shard)
+        _lib.decdec_linear_p2p(self.lin.struct, x.data_ptr(), k, chunk, self.y_off, self.slot,
+                               sel.data_ptr() if sel is not None else 0, workspace.ptr, workspace.nbytes,
+                               self.peers.handle, _stream_ptr(stream))
+        return self.y_full
+
+
+class P2PStack:
+    """A TP decode step with the fused all-gather (decdec_stack_create_p2p): layer i writes every
+    rank's y_full at y_offs[i] and waits on slot i; one native CUDA graph, no collective launch."""
+
+    def __init__(self, layers, ks, xs, y_offs, workspace, peers: Peers, chunk: int = 0):
+        from paper_2412_20185_b200 import _lib
+
+        self._lib = _lib
+        self._keep = (list(layers), list(xs), workspace, peers)
+        self.handle = _lib.decdec_stack_create_p2p([l.struct for l in layers], ks, chunk, [x.data_ptr() for x in xs],
+                                                   list(y_offs), workspace.ptr, workspace.nbytes, peers.handle, 0)
+        self.kernels = _lib.decdec_stack_kernels(self.handle)
+        self.y_full = [peers.view(o, l.d_out * peers.world) for o, l in zip(y_offs, layers)]
+
+    def launch(self, stream=None):
+        from paper_2412_20185_b200.layer import _stream_ptr
+
+        self._lib.decdec_stack_launch(self.handle, _stream_ptr(stream))
+
+    def close(self):
+        if self.handle:
+            self._lib.decdec_stack_destroy(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -96,3 +96,17 @@ def test_num_selected_and_workspace(dd):
     assert dd.decdec_num_selected(4096, 2000, 1024) == -1
     # the paper's k x (4+2) B buffer is part of the workspace
     assert dd.decdec_workspace_bytes(1433, 4096) >= 1433 * 6
+
+
+def test_peer_offsets_symmetric_layout():
+    """Fused P2P all-gather: y_full buffers of a stack in the peer user area (tp.peer_offsets)
+    are 256-B aligned, disjoint and in layer order -- the same offsets on every rank."""
+    from paper_2412_20185_b200.tp import peer_offsets
+
+    d_outs = [768, 512, 3584, 512]
+    for world in (1, 2, 8):
+        offs, total = peer_offsets(d_outs, world)
+        ends = [o + world * d * 2 for o, d in zip(offs, d_outs)]
+        assert all(o % 256 == 0 for o in offs)
+        assert all(e <= o2 for e, o2 in zip(ends, offs[1:]))
+        assert total >= ends[-1] and total % 256 == 0
