@@ -494,33 +494,43 @@ def main():
                                               hbm_peak, pcie_peak)}
             del M4
 
-    # ---- NEXT-3: the same stack with a non-uniform (LUT) base, k_chunk 0 (compensation on LUT
-    # layers is not built) -------------------------------------------------------------------
+    # ---- NEXT-3: the same stack with a non-uniform (LUT) base: k_chunk 0 (k_gemv16) and the
+    # headline k_chunk (fused kernel with the LUT base + compensation, same host residual) -----
     lut = None
     if not (args.quick or args.sweep_only or args.no_lut) and world == 1:
         from synth import gen_perf_layer_lut_device
         lut = {"config": "Llama-3-8B, SqueezeLLM-style per-column fp16 table of 2^b entries (P:397, P:502), "
-                         "W4K nibble codes, k_chunk 0 (uncompensated base GEMV, k_gemv16)"}
+                         f"W4K nibble codes; k_chunk 0 (base GEMV, k_gemv16) and {args.kchunk} (fused kernel, "
+                         "LUT base + r4 compensation from the same host residual store)"}
+        lut_sweep = sorted({0, args.kchunk})
         for lb in (3, 4):
             ML = Model.__new__(Model)
-            ML.layers, ML.meta, ML.hosts, ML.n_blocks = [], [], [], M.n_blocks
-            for (b, name, d_in, d_out) in M.meta:
+            ML.layers, ML.meta, ML.hosts, ML.n_blocks = [], [], M.hosts, M.n_blocks
+            for li, (b, name, d_in, d_out) in enumerate(M.meta):
                 g = gen_perf_layer_lut_device(d_in, d_out, lb, layer_seed("lut", args.model, b, name))
-                ML.layers.append(dd.QuantLinear.from_device_lut(d_in, d_out, lb, g["w"], g["lut"]))
+                ML.layers.append(dd.QuantLinear.from_device_lut(d_in, d_out, lb, g["w"], g["lut"], host=M.hosts[li],
+                                                                host_scales_off=M.layers[li].host_scales_off))
                 ML.meta.append((b, name, d_in, d_out))
             ML.x_off, ML.y_off, ML.x_host, ML.x_dev, ML.y_dev = M.x_off, M.y_off, M.x_host, M.x_dev, M.y_dev
             ML.max_d_out, ML.max_d_in = M.max_d_out, M.max_d_in
-            rl = step_sweep(torch, dist, dd, ML, ws, [0], args.steps, args.warmup, stream, world)
-            # bytes per call: 4-bit codes + fp16 table of 2^b per row + x + y
-            per = time_shapes(torch, dist, dd, ML, ws, [0], args.steps, stream, world, 4, hbm_peak, pcie_peak)
+            rl = step_sweep(torch, dist, dd, ML, ws, lut_sweep, args.steps, args.warmup, stream, world)
+            # bytes per call: 4-bit codes + fp16 table of 2^b per row + x + y (+ PCIe as the uniform base)
+            per = time_shapes(torch, dist, dd, ML, ws, lut_sweep, args.steps, stream, world, 4, hbm_peak, pcie_peak)
             for n_, v_ in per.items():
                 d_in, d_out = v_["d_in"], v_["d_out"]
                 bh = d_in * d_out // 2 + d_out * (2 << lb) + 2 * d_in + 2 * d_out
-                e0 = v_["0"]
-                e0["hbm_GBps"] = round(bh / e0["us"] / 1e3, 1)
-                e0["roofline_us"] = round(bh / (hbm_peak * 1e3), 3)
-                e0["roofline_frac"] = e0["hbm_frac"] = round(bh / (hbm_peak * 1e3) / e0["us"], 3)
-            lut[f"b{lb}"] = {"tokens_per_s": round(rl[0]["tokens_per_s"], 2), "ms_per_step": round(rl[0]["ms_per_step"], 4),
+                for key, e0 in v_.items():
+                    if not isinstance(e0, dict):
+                        continue
+                    bp = (e0["k"] * d_out // 2 + 2 * d_out) if e0["k"] else 0
+                    t_roof = max(bh / (hbm_peak * 1e3), bp / (pcie_peak * 1e3))
+                    e0["hbm_GBps"] = round(bh / e0["us"] / 1e3, 1)
+                    e0["roofline_us"] = round(t_roof, 3)
+                    e0["roofline_frac"] = round(t_roof / e0["us"], 3)
+                    e0["hbm_frac"] = round(bh / (hbm_peak * 1e3) / e0["us"], 3)
+            lut[f"b{lb}"] = {"sweep": {str(k): {"tokens_per_s": round(v["tokens_per_s"], 2), "ms_per_step": round(v["ms_per_step"], 4)}
+                                       for k, v in rl.items()},
+                             "tokens_per_s": round(rl[0]["tokens_per_s"], 2), "ms_per_step": round(rl[0]["ms_per_step"], 4),
                              "per_layer_us": per}
             del ML
 

@@ -69,8 +69,9 @@ typedef enum {
  * w_format = DECDEC_WFMT_LUT (the paper's non-uniform base, SqueezeLLM served by a LUT kernel,
  * P:397): W_hat[i][j] = w_lut[j][q_ij], codes q < 2^w_bits
  * (w_bits = 3 | 4) packed as W4K nibbles (4 bits per weight for both widths), no s / z
- * (w_scales / w_zeros unused).  Tables: fp16 [d_out][2^w_bits].  Compensation (k > 0) is
- * not implemented for LUT layers yet: DECDEC_EUNSUPPORTED.
+ * (w_scales / w_zeros unused).  Tables: fp16 [d_out][2^w_bits].  Compensation (k > 0) runs
+ * in the same fused kernel (rows' tables staged in place of the scales) with r_bits = 4 only;
+ * r_bits = 16 on a LUT layer: DECDEC_EUNSUPPORTED.
  * Residual R_hat = S_j * c_ij, c in [-7, 7]: rows = input channels,
  * contiguous, in HOST MAPPED memory (zero-copy):
  *   r_bits = 4  (layout Rq):  uint32 [d_in][d_out/8], nibble = c + 8, column c of an

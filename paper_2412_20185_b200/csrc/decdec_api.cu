@@ -131,13 +131,19 @@ bool plan_dec(int d_out, int k_sel, int sel_len, int warps, int max_rpi, double 
   return false;
 }
 
-decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int sel_len = 0, int r_bits = 4) {
+// lut_bits = 3 | 4: non-uniform base (W4K nibble codes + a 2^lut_bits fp16 table per row in
+// place of the group scales / zeros)
+decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int sel_len = 0, int r_bits = 4,
+                        int lut_bits = 0) {
   if (sel_len == 0) sel_len = d_in;
   const int G = d_in / DECDEC_GROUP;
   const int sms = device_sms();
   const bool small_g = G <= 32 && 32 % G == 0;
   const int nkw = small_g ? 0 : (G + 31) / 32;
+  if (lut_bits) bits = 4;  // codes are W4K nibbles
   const uint32_t row_bytes = (uint32_t)d_in * bits / 8;
+  const uint32_t meta_row = lut_bits ? (2u << lut_bits) : (uint32_t)G * 2;  // scale / table bytes per row
+  const uint32_t zero_row = lut_bits ? 0u : (uint32_t)G;
   static int env_nc = -1, env_rps = -1;
   if (env_nc < 0) {
     const char* e = getenv("DECDEC_PLAN");
@@ -146,7 +152,7 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
     if (e) sscanf(e, "%d,%d", &env_nc, &env_rps);
   }
   // PCIe / HBM roofline time ratio with the measured link and copy bandwidths
-  const double t_hbm = ((double)d_in * d_out * bits / 8 + 3.0 * d_out * G) / 6455.0;
+  const double t_hbm = ((double)d_in * d_out * bits / 8 + (double)d_out * (meta_row + zero_row)) / 6455.0;
   const double t_pcie = ((double)k_sel * d_out * r_bits / 8 + 2.0 * d_out) / 51.4;
   const double r_ratio = t_pcie / t_hbm;
   Plan best{};
@@ -165,8 +171,8 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
       p.TR = p.NSLOTS * rps;
       if (p.TR > kSegCols || kSegCols % p.TR || d_out % p.TR || (p.TR * G) % 16) continue;
       p.off_s = (uint32_t)p.TR * row_bytes;
-      p.off_z = p.off_s + (uint32_t)p.TR * G * 2;
-      p.stage_bytes = (uint32_t)align_up(p.off_z + (uint32_t)p.TR * G, 16);
+      p.off_z = p.off_s + (uint32_t)p.TR * meta_row;
+      p.stage_bytes = (uint32_t)align_up(p.off_z + (uint32_t)p.TR * zero_row, 16);
       const size_t red = (size_t)2 * p.NSLOTS * 4 * (nkw ? nkw : 1) * 4;
       const size_t xb = align_up((size_t)d_in * 2, 16);  // staged x (swizzled, see k_linear)
       const size_t avail = kSmemBudget - red - 16 * 8 - xb;
@@ -356,6 +362,8 @@ decdec_status init_attrs() {
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 16>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 16>, lin);
+  if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4, 3>, lin);
+  if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4, 4>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<3, 0>, kGemvSmemBudget + 1024);
   if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<4, 0>, kGemvSmemBudget + 1024);
   if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<3, 1>, kGemvSmemBudget + 1024);
@@ -400,15 +408,15 @@ decdec_status check_layer(const decdec_layer* L, bool need_residual) {
   if (L->d_in < 128 || L->d_in > 32768 || L->d_in % DECDEC_GROUP) return DECDEC_EINVAL;
   if (L->d_out < 32 || L->d_out % 32) return DECDEC_EINVAL;
   if (L->w_format == DECDEC_WFMT_LUT) {
-    if (need_residual) return DECDEC_EUNSUPPORTED;  // LUT + compensation: not built yet
     if (!L->w_packed || !L->w_lut) return DECDEC_EINVAL;
     if (!aligned16(L->w_packed) || !aligned16(L->w_lut)) return DECDEC_EALIGN;
     if (!is_device_ptr(L->w_packed) || !is_device_ptr(L->w_lut)) return DECDEC_EINVAL;
-    return DECDEC_OK;
+    if (need_residual && L->r_bits != 4) return DECDEC_EUNSUPPORTED;  // LUT base: r4 residual only
+  } else {
+    if (!L->w_packed || !L->w_scales || !L->w_zeros) return DECDEC_EINVAL;
+    if (!aligned16(L->w_packed) || !aligned16(L->w_scales) || !aligned16(L->w_zeros)) return DECDEC_EALIGN;
+    if (!is_device_ptr(L->w_packed) || !is_device_ptr(L->w_scales) || !is_device_ptr(L->w_zeros)) return DECDEC_EINVAL;
   }
-  if (!L->w_packed || !L->w_scales || !L->w_zeros) return DECDEC_EINVAL;
-  if (!aligned16(L->w_packed) || !aligned16(L->w_scales) || !aligned16(L->w_zeros)) return DECDEC_EALIGN;
-  if (!is_device_ptr(L->w_packed) || !is_device_ptr(L->w_scales) || !is_device_ptr(L->w_zeros)) return DECDEC_EINVAL;
   if (need_residual) {
     if (L->r_bits != 4 && L->r_bits != 16) return DECDEC_EUNSUPPORTED;
     if (!L->r_rows || (L->r_bits == 4 && !L->r_scales)) return DECDEC_EINVAL;
@@ -452,7 +460,7 @@ bool coop_launch() {
   return env == 1;
 }
 
-template <int BITS, int RBITS>
+template <int BITS, int RBITS, int LUTB = 0>
 decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pl.grid);
@@ -475,10 +483,13 @@ decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, c
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  return cuda_status(cudaLaunchKernelEx(&cfg, k_linear<BITS, RBITS>, p));
+  return cuda_status(cudaLaunchKernelEx(&cfg, k_linear<BITS, RBITS, LUTB>, p));
 }
 
-decdec_status launch_linear(const LinearParams& p, const Plan& pl, int bits, int rbits, bool pdl, cudaStream_t st) {
+decdec_status launch_linear(const LinearParams& p, const Plan& pl, int bits, int rbits, bool pdl, cudaStream_t st,
+                            int lut_bits = 0) {
+  if (lut_bits == 3) return launch_linear_t<4, 4, 3>(p, pl, pdl, st);  // LUT base: W4K nibbles, r4 residual
+  if (lut_bits == 4) return launch_linear_t<4, 4, 4>(p, pl, pdl, st);
   if (bits == 3) return rbits == 16 ? launch_linear_t<3, 16>(p, pl, pdl, st) : launch_linear_t<3, 4>(p, pl, pdl, st);
   return rbits == 16 ? launch_linear_t<4, 16>(p, pl, pdl, st) : launch_linear_t<4, 4>(p, pl, pdl, st);
 }
@@ -528,15 +539,16 @@ bool use_gemv_kernel() {
 
 LinearParams base_params(const decdec_layer* L, const uint16_t* x, uint16_t* y, const Plan& pl) {
   LinearParams p{};
+  const bool lut = L->w_format == DECDEC_WFMT_LUT;
   p.w = static_cast<const uint8_t*>(L->w_packed);
-  p.ws = L->w_scales;
-  p.wz = L->w_zeros;
+  p.ws = lut ? L->w_lut : L->w_scales;  // LUT base: the rows' tables travel in the scales' place
+  p.wz = lut ? nullptr : L->w_zeros;
   p.x = x;
   p.y = y;
   p.d_in = L->d_in;
   p.d_out = L->d_out;
   p.G = pl.G;
-  p.row_bytes = L->d_in * L->w_bits / 8;
+  p.row_bytes = L->d_in * (lut ? 4 : L->w_bits) / 8;
   p.TR = pl.TR;
   p.NKW = pl.NKW;
   p.NSLOTS = pl.NSLOTS;
@@ -689,9 +701,10 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
     return DECDEC_OK;
   }
   const int sel_len = chunk ? (chunk < L->d_in ? chunk : L->d_in) : L->d_in;
-  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &P.pl, sel_len, L->r_bits)) != DECDEC_OK)
+  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &P.pl, sel_len, L->r_bits, lutb)) != DECDEC_OK)
     return s;
   P.p = base_params(L, x, y, P.pl);
+  P.lut_bits = lutb;
   P.k = k;
   P.chunk = chunk;
   P.bits = L->w_bits;
@@ -727,7 +740,7 @@ decdec_status enqueue_linear(const Prepared& P, cudaStream_t st, bool chained = 
   if (P.gemv) return launch_gemv(P.gpl, P.bits, chained, st, P.lut_bits);
   Plan pl = P.pl;
   pl.grid += P.pl.n_dec;  // DEC CTAs first
-  return launch_linear(P.p, pl, P.bits, P.p.k_sel ? P.rbits : 4, chained, st);
+  return launch_linear(P.p, pl, P.bits, P.p.k_sel ? P.rbits : 4, chained, st, P.lut_bits);
 }
 
 // This rank's shard pointer inside the user area of its peer region (decdec_linear_p2p).
@@ -955,7 +968,7 @@ decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, si
     return DECDEC_OK;
   }
   Plan pl;
-  decdec_status s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &pl);
+  decdec_status s = make_plan(L->d_in, L->d_out, L->w_bits, k_sel, &pl, 0, L->r_bits ? L->r_bits : 4, lutb);
   if (s != DECDEC_OK) return s;
   snprintf(buf, buf_bytes,
            "{\"G\": %d, \"NKW\": %d, \"NSLOTS\": %d, \"RPS\": %d, \"TR\": %d, \"NC\": %d, \"n_dec\": %d, "

@@ -90,32 +90,6 @@ __device__ __forceinline__ float row_group_dot(const uint8_t* gp, const uint32_t
   return s24 * fmaf(-z, Xs, combine_classes<BITS>(a));
 }
 
-// LUT base (NEXT-3): one row's partial sum_{i in g} lut[q_i] x_i for input group g.  gp: the
-// group's 64 B of W4K nibble codes; lp: the row's table (2^LB fp16) in smem; xr: x in the
-// (c, c+2) pairing of lut_x_pairs.
-template <int LB>
-__device__ __forceinline__ float row_group_dot_lut(const uint8_t* gp, const uint32_t* lp, const uint32_t* xr, int rot) {
-  uint32_t e[1 << (LB - 1)], tl[(1 << LB) / 4], th[(1 << LB) / 4];
-#pragma unroll
-  for (int t = 0; t < (1 << LB) / 8; ++t) {
-    const uint4 v = reinterpret_cast<const uint4*>(lp)[t];
-    e[4 * t] = v.x; e[4 * t + 1] = v.y; e[4 * t + 2] = v.z; e[4 * t + 3] = v.w;
-  }
-  lut_planes<LB>(e, tl, th);
-  float a[4] = {0.f, 0.f, 0.f, 0.f};
-  uint4 v[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const uint4*>(gp + 16 * ((j + rot) & 3));
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    fma_lut_word<LB>(v[j].x, tl, th, xr + 16 * j + 0, a);
-    fma_lut_word<LB>(v[j].y, tl, th, xr + 16 * j + 4, a);
-    fma_lut_word<LB>(v[j].z, tl, th, xr + 16 * j + 8, a);
-    fma_lut_word<LB>(v[j].w, tl, th, xr + 16 * j + 12, a);
-  }
-  return (a[0] + a[1]) + (a[2] + a[3]);
-}
-
 // Two rows at once (12 independent FHFMA chains; x registers shared): more ILP per warp.
 template <int BITS>
 __device__ __forceinline__ void row_group_dot2(const uint8_t* g0, const uint8_t* g1, const uint32_t* xr, float Xs, float s0,

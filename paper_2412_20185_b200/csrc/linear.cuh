@@ -371,7 +371,10 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   }
 }
 
-template <int BITS, int RBITS>
+// LUTB = 0: uniform base (W3K / W4K codes, per-group fp16 scale + u8 zero); LUTB = 3 | 4: the
+// non-uniform base (NEXT-3, P:397 / P:502): W4K nibble codes (BITS = 4) and, in place of the
+// scales, each row's table of 2^LUTB fp16 values; no zeros.
+template <int BITS, int RBITS, int LUTB = 0>
 __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stage0 = smem;
@@ -411,7 +414,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      const uint32_t wb = (uint32_t)p.TR * p.row_bytes, sb = (uint32_t)p.TR * p.G * 2, zb = (uint32_t)p.TR * p.G;
+      const uint32_t wb = (uint32_t)p.TR * p.row_bytes;
+      const uint32_t sb = LUTB ? (uint32_t)p.TR * (2u << LUTB) : (uint32_t)p.TR * p.G * 2;  // scales | tables
+      const uint32_t zb = LUTB ? 0u : (uint32_t)p.TR * p.G;
       const int stages = p.stages;
       int it = 0, st = 0;
       uint32_t ph = 0;  // phase of the current pass over the ring
@@ -430,8 +435,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
         uint8_t* dst = stage0 + (size_t)st * p.stage_bytes;
         mbar_arrive_expect_tx(&full[st], wb + sb + zb);
         bulk_g2s(dst, p.w + (size_t)tile * wb, wb, &full[st], pol);
-        bulk_g2s(dst + p.off_s, p.ws + (size_t)tile * p.TR * p.G, sb, &full[st], pol);
-        bulk_g2s(dst + p.off_z, p.wz + (size_t)tile * p.TR * p.G, zb, &full[st], pol);
+        bulk_g2s(dst + p.off_s, p.ws + (size_t)tile * p.TR * (LUTB ? (1 << LUTB) : p.G), sb, &full[st], pol);
+        if (!LUTB) bulk_g2s(dst + p.off_z, p.wz + (size_t)tile * p.TR * p.G, zb, &full[st], pol);
         if (++st == stages) {
           st = 0;
           ph ^= 1;
@@ -498,6 +503,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       Xs = ((xa[0] + xa[1]) + (xa[2] + xa[3])) + ((xa[4] + xa[5]) + (xa[6] + xa[7]));
 #endif
       Xs *= 5.9604644775390625e-08f;  // 2^-24: same scale as the decoded codes
+      if (LUTB) {
+#pragma unroll
+        for (int w = 0; w < 16; ++w) lut_x_pairs(xr + 4 * w);  // (c, c+2) pairing of the table lookups
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 64; ++i) xr[i] = 0u;
@@ -532,6 +541,15 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
         if (active) {
           const uint8_t* g0 = sw + r0 * row_bytes + g * GB;
           float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (LUTB) {
+            const float v = row_group_dot_lut<LUTB ? LUTB : 3>(
+                g0, reinterpret_cast<const uint32_t*>(sw + p.off_s + (size_t)r0 * (2 << LUTB)), xr, rot);
+            part[0] = m == 0 ? v : part[0];
+            part[1] = m == 1 ? v : part[1];
+            part[2] = m == 2 ? v : part[2];
+            part[3] = m == 3 ? v : part[3];
+            continue;
+          }
           if (BITS == 4) {
             uint4 v0[4];
 #pragma unroll
@@ -573,6 +591,15 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
           const uint8_t* g0 = sw + r0 * row_bytes + g * GB;
           const uint8_t* g1 = sw + (two ? r1 : r0) * row_bytes + g * GB;
           float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, a1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (LUTB) {  // non-uniform base: sum_i lut[q_i] x_i per row, no scale / zero
+            const uint8_t* tb = sw + p.off_s;
+            part[m] = row_group_dot_lut<LUTB ? LUTB : 3>(g0, reinterpret_cast<const uint32_t*>(tb + (size_t)r0 * (2 << LUTB)),
+                                                         xr, rot);
+            if (two)
+              part[m + 1] = row_group_dot_lut<LUTB ? LUTB : 3>(
+                  g1, reinterpret_cast<const uint32_t*>(tb + (size_t)r1 * (2 << LUTB)), xr, rot);
+            continue;
+          }
           if (BITS == 4) {
             uint4 v0[4], v1[4];
 #pragma unroll

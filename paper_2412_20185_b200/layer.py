@@ -93,6 +93,13 @@ class QuantLinear:
         self.w = torch.from_numpy(wp.view(np.uint8).reshape(-1)).to(device)
         self.s = torch.from_numpy(np.ascontiguousarray(np.asarray(s, np.float16).T).reshape(-1)).to(device)
         self.z = torch.from_numpy(np.ascontiguousarray(np.asarray(z, np.uint8).T).reshape(-1)).to(device)
+        self._attach_residual(rc, rS, r16, numa_node)
+        self._L = self._struct()
+        return self
+
+    def _attach_residual(self, rc=None, rS=None, r16=None, numa_node=-1):
+        """R_hat into pinned + mapped host memory: Rq rows + fp16 scales (r_bits 4) or fp16 rows."""
+        d_in, d_out = self.d_in, self.d_out
         self.r_bits = 0
         if rc is not None:
             self.r_bits = 4
@@ -107,14 +114,12 @@ class QuantLinear:
             self.r_bits = 16
             self.host = HostBuffer(d_in * d_out * 2, numa_node)
             self.host.numpy(np.float16, (d_in, d_out))[:] = np.asarray(r16, np.float16)
-        self._L = self._struct()
-        return self
 
     @classmethod
-    def from_lut_codes(cls, q, lut, bits, device="cuda"):
+    def from_lut_codes(cls, q, lut, bits, rc=None, rS=None, device="cuda", numa_node=-1):
         """Non-uniform (LUT) base layer (NEXT-3): q uint8 [d_in, d_out] codes < 2^bits, lut fp16
         [2^bits, d_out] (oracle layout).  Codes are packed as W4K nibbles by the C++ packer; the
-        device table is [d_out][2^bits]."""
+        device table is [d_out][2^bits].  Optional r4 residual rc / rS as in from_codes."""
         self = cls()
         q = np.asarray(q)
         d_in, d_out = q.shape
@@ -122,19 +127,20 @@ class QuantLinear:
         self.w = torch.from_numpy(pack_weights(q, 4).view(np.uint8).reshape(-1)).to(device)
         self.lut = torch.from_numpy(np.ascontiguousarray(np.asarray(lut, np.float16).T).reshape(-1)).to(device)
         self.s = self.z = None
-        self.r_bits = 0
         self.w_format = 1
+        self._attach_residual(rc, rS, None, numa_node)
         self._L = self._struct()
         return self
 
     @classmethod
-    def from_device_lut(cls, d_in, d_out, bits, w, lut):
+    def from_device_lut(cls, d_in, d_out, bits, w, lut, host=None, host_scales_off=0):
         """Wrap device tensors of a LUT layer (perf harness): w uint8 W4K nibbles [d_out*d_in/2],
-        lut fp16 [d_out * 2^bits]."""
+        lut fp16 [d_out * 2^bits]; host: optional HostBuffer with Rq rows + scales (r4)."""
         self = cls()
         self.d_in, self.d_out, self.bits = d_in, d_out, bits
         self.w, self.lut, self.s, self.z = w, lut, None, None
-        self.r_bits, self.w_format = 0, 1
+        self.w_format = 1
+        self.host, self.r_bits, self.host_scales_off = host, (4 if host is not None else 0), host_scales_off
         self._L = self._struct()
         return self
 

@@ -314,40 +314,55 @@ def test_r16_llama_o_shape():
 # ------------------------------------------------------------------ NEXT-3: non-uniform (LUT) base
 @pytest.mark.parametrize("bits", [3, 4])
 def test_lut_config1_full_pipeline(bits):
-    """SqueezeLLM-style LUT base (ledger L17): seeded fp16 W -> oracle k-means
-    tables -> the LUT GEMV kernel, every output column within L9; codes decoded bit-exact."""
+    """SqueezeLLM-style LUT base (ledger L17) with DecDEC compensation: seeded fp16
+    W -> oracle k-means tables -> residual R = W - W_hat (O2) -> Q_r (O3) -> the LUT GEMV kernel
+    (k = 0) and the fused kernel with the LUT base (k = 16, the compensation of P:204-207):
+    every output column within L9, selection bit-exact, codes decoded bit-exact."""
     d_in, d_out = SHAPES["config1"]["l"]
     W = gen_weight_fp16(d_in, d_out, layer_seed("lut", "W", bits))
     q, lut = oracle.quantize_base_lut(W, bits)
-    lin = dd.QuantLinear.from_lut_codes(q, lut, bits)
+    rc, rS = quantize_residual(residual(W, oracle.dequantize_lut(q, lut)), 4)
+    lin = dd.QuantLinear.from_lut_codes(q, lut, bits, rc=rc, rS=rS)
     assert np.array_equal(lin.debug_unpack().cpu().numpy(), q.T)
-    plan = _plan(lin, 0)
-    assert plan["kernel"] == "k_gemv"
+    assert _plan(lin, 0)["kernel"] == "k_gemv"
+    assert "n_dec" in _plan(lin, 16)  # k > 0: the fused kernel (DEC CTAs + LUT GEMV CTAs)
+    ws = dd.Workspace(64, d_out)
     X = gen_activations(d_in, 4, seed=layer_seed("lut", "x", bits))
     for xi, x in enumerate(X):
         y = lin(to_dev(x), 0)
         ref = decdec_linear_ref(q, None, None, x, 0, lut=lut)
         check_full(y, ref, f"lut/config1/b{bits}/x{xi}")
         assert torch.equal(y, lin.gemv(to_dev(x)))
-    with pytest.raises(dd.DecdecError) as e:   # compensation on LUT layers: not built (header)
-        lin(to_dev(X[0]), 16, workspace=dd.Workspace(16, d_out))
-    assert e.value.status == -4
+        for k in (16, 64):
+            sel = torch.empty(k, dtype=torch.int32, device=DEV)
+            y = lin(to_dev(x), k, sel=sel, workspace=ws)
+            ref = decdec_linear_ref(q, None, None, x, k, rc=rc, rS=rS, lut=lut)
+            assert np.array_equal(sel.cpu().numpy(), ref["idx"])
+            check_full(y, ref, f"lut/config1/b{bits}/k{k}/x{xi}")
 
 
 @pytest.mark.parametrize("bits", [3, 4])
 @pytest.mark.parametrize("model,name", [("llama3_8b", "qkv"), ("llama3_8b", "o"), ("llama3_8b", "gu"),
                                         ("llama3_8b", "d"), ("phi3_medium", "o"), ("phi3_medium", "d")])
 def test_lut_shapes_all_columns(bits, model, name):
+    """LUT base at full Llama-3-8B / Phi-3 shapes, k_chunk 0 (k_gemv16) and 21 (fused kernel with
+    the LUT base + compensation): every output column, selection bit-exact."""
     from synth import gen_perf_layer_lut
 
     d_in, d_out = SHAPES[model][name]
-    L = gen_perf_layer_lut(d_in, d_out, bits, seed=layer_seed("lutperf", model, name, bits), with_residual=False)
-    lin = dd.QuantLinear.from_lut_codes(L["q"], L["lut"], bits)
+    L = gen_perf_layer_lut(d_in, d_out, bits, seed=layer_seed("lutperf", model, name, bits))
+    lin = dd.QuantLinear.from_lut_codes(L["q"], L["lut"], bits, rc=L["rc"], rS=L["rS"])
     W_hat = oracle.dequantize_lut(L["q"], L["lut"])
     x = gen_activations(d_in, 1, seed=layer_seed("lutperf", name, "x"), kind="d" if name == "d" else "qkv")[0]
-    y = lin(to_dev(x), 0)
-    ref = decdec_linear_ref(L["q"], None, None, x, 0, W_hat=W_hat)
-    check_full(y, ref, f"lut/{model}/{name}/b{bits}")
+    ws = dd.Workspace(oracle.k_from_kchunk(21, d_in), d_out)
+    for kc in (0, 21):
+        k = oracle.k_from_kchunk(kc, d_in)
+        sel = torch.empty(max(k, 1), dtype=torch.int32, device=DEV)
+        y = lin(to_dev(x), k, sel=sel if k else None, workspace=ws)
+        ref = decdec_linear_ref(L["q"], None, None, x, k, rc=L["rc"], rS=L["rS"], W_hat=W_hat)
+        if k:
+            assert np.array_equal(sel.cpu().numpy(), ref["idx"])
+        check_full(y, ref, f"lut/{model}/{name}/b{bits}/kc{kc}")
 
 
 @pytest.mark.parametrize("kind", ["all_equal", "zeros", "ties", "sparse"])

@@ -1,6 +1,7 @@
+python paper_2412_20185_b200/build.py; mkdir -p gpurun_out; export DECDEC_PARITY_REPORT=gpurun_out/final_parity_report.json
 # Round-end measurement set (run on the GPU box): GPU tests, smoke, bench + reference arm,
 # ncu launch list, ncu --set full of the gu layer at k_chunk 0/21, stack timeline -> gpurun_out/final_*
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/final_pytest.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/final_pytest_full.txt 2>&1; tail -3 gpurun_out/final_pytest_full.txt > gpurun_out/final_pytest.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.txt 2>&1
 timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/final_bench_ref.json 2> gpurun_out/final_bench_ref.err
