@@ -573,7 +573,7 @@ def main():
         traffic = None
         if shard == 1 and args.model == "llama3_8b" and args.bits == 3:  # the captured layer's shape only
             try:
-                with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+                with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
                     traffic = json.load(f).get(f"{dom}/{args.kchunk}")
             except Exception:
                 pass
