@@ -528,6 +528,19 @@ bool l2_next_prefetch() {
 // Llama-3-8B 3-bit k_chunk-0 step, profiles/r02_gemv_ab.json): k_linear 1.078 ms; k_gemv16
 // 1.25-1.32 ms (dedicated or in-warp producer, single rows or pairs, 16-96 KB before the wait),
 // two-CTAs-per-SM k_gemv 1.44-1.51 ms.  LUT (non-uniform) layers always use k_gemv16.
+// LUT-base k = 0 calls: the fused kernel's GEMV CTAs or k_gemv16.  Measured (Llama-3-8B k_chunk-0
+// step, 1x B200, profiles/r02_experiments.json): 3-bit tables 1.443 ms fused vs 1.586 ms k_gemv16;
+// 4-bit tables 2.252 vs 2.118 (k_linear<4,4,4> spills its table planes).  DECDEC_LUT_GEMV16=0|1
+// forces one kernel for both widths.
+bool lut_gemv16(int lutb) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("DECDEC_LUT_GEMV16");
+    env = e ? (atoi(e) > 0) : -1;
+  }
+  return env >= 0 ? env == 1 : lutb == 4;
+}
+
 bool use_gemv_kernel() {
   static int env = -1;
   if (env < 0) {
@@ -634,7 +647,7 @@ decdec_status decdec_gemv(const decdec_layer* L, const uint16_t* x, uint16_t* y,
   if (!aligned16(x) || !aligned16(y)) return DECDEC_EALIGN;
   if ((s = ensure_attrs()) != DECDEC_OK) return s;
   const int lutb = L->w_format == DECDEC_WFMT_LUT ? L->w_bits : 0;
-  if (use_gemv_kernel() || lutb) {
+  if (use_gemv_kernel() || (lutb && lut_gemv16(lutb))) {
     GemvPlan gpl;
     if ((s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &gpl, lutb)) != DECDEC_OK) return s;
     gpl.gp.w = static_cast<const uint8_t*>(L->w_packed);
@@ -646,9 +659,9 @@ decdec_status decdec_gemv(const decdec_layer* L, const uint16_t* x, uint16_t* y,
     return launch_gemv(gpl, L->w_bits, false, (cudaStream_t)stream, lutb);
   }
   Plan pl;
-  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, 0, &pl)) != DECDEC_OK) return s;
+  if ((s = make_plan(L->d_in, L->d_out, L->w_bits, 0, &pl, 0, 4, lutb)) != DECDEC_OK) return s;
   LinearParams p = base_params(L, x, y, pl);
-  return launch_linear(p, pl, L->w_bits, 4, false, (cudaStream_t)stream);
+  return launch_linear(p, pl, L->w_bits, 4, false, (cudaStream_t)stream, lutb);
 }
 
 }  // extern "C"
@@ -679,7 +692,7 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
   if ((s = ensure_attrs()) != DECDEC_OK) return s;
   Prepared P{};
   const int lutb = L->w_format == DECDEC_WFMT_LUT ? L->w_bits : 0;
-  if (k_sel == 0 && (use_gemv_kernel() || lutb)) {
+  if (k_sel == 0 && (use_gemv_kernel() || (lutb && lut_gemv16(lutb)))) {
     if ((s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &P.gpl, lutb)) != DECDEC_OK) return s;
     GemvParams& g = P.gpl.gp;
     g.w = static_cast<const uint8_t*>(L->w_packed);
@@ -956,7 +969,7 @@ decdec_status decdec_plan_string(const decdec_layer* L, int32_t k, char* buf, si
   if (!L || !buf) return DECDEC_EINVAL;
   const int k_sel = k;  // caller passes the selected count
   const int lutb = L->w_format == DECDEC_WFMT_LUT ? L->w_bits : 0;
-  if (k_sel == 0 && (use_gemv_kernel() || lutb)) {
+  if (k_sel == 0 && (use_gemv_kernel() || (lutb && lut_gemv16(lutb)))) {
     GemvPlan g;
     decdec_status s = make_gemv_plan(L->d_in, L->d_out, L->w_bits, device_sms(), &g, lutb);
     if (s != DECDEC_OK) return s;
