@@ -239,6 +239,26 @@ decdec_status decdec_stack_create_p2p(const decdec_layer* layers, int32_t n_laye
                                       const uint16_t* const* x, const size_t* y_off, void* ws, size_t ws_bytes,
                                       decdec_peers* peers, decdec_stream_t stream, decdec_stack** out);
 
+/* ---- multi-link residual fetch (the analogue of the paper's GH200
+ * C2C observation): when peer GPUs are idle (no tensor parallelism), a layer's
+ * residual gather is split across their PCIe links.  Every rank of a decdec_peers group calls
+ * decdec_linear_ml with the same layer (same packed residual contents in its own host-mapped
+ * memory; the base weights are read on rank 0 only), x, k and chunk.  Every rank computes the
+ * identical selection S; rank r fetches the positions p of S with p % nranks == r, and the helper
+ * ranks (r > 0) store their o_dec parts (fp32, times S_j) into rank 0's user area over NVLink;
+ * rank 0 runs the base GEMV, its own share, and adds the helpers' parts in rank order before
+ * writing y.  Handshake per DEC CTA (flag + ack words in the user area at ml_off, the same
+ * offset on every rank, decdec_ml_bytes(d_out, nranks) bytes): a helper writes only after rank 0
+ * consumed its previous part, so consecutive calls need no other synchronisation.  y / sel are
+ * rank 0's (helpers: ignored, may be NULL).  k = 0 or a single rank: rank 0 runs decdec_linear
+ * alone and helpers return at once.  Errors as decdec_linear; DECDEC_EINVAL (group not
+ * connected, ml_off not 16-B aligned), DECDEC_ESPACE (ml area outside the user area),
+ * DECDEC_EUNSUPPORTED (more than 64 DEC CTAs).  A peer that never arrives traps after ~20 s. */
+size_t decdec_ml_bytes(int32_t d_out, int32_t nranks);
+decdec_status decdec_linear_ml(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk, uint16_t* y,
+                               int32_t* sel, void* ws, size_t ws_bytes, decdec_peers* peers, size_t ml_off,
+                               decdec_stream_t stream);
+
 /* ------------------------------------------------------------------ offline, host-only */
 /* Pack base codes q (u8 [d_in][d_out], logical W layout, values < 2^bits) into W3K/W4K
  * (uint32 [d_out][d_in*bits/32]).  out_bytes must be >= d_out*d_in*bits/8. */

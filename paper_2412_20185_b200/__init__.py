@@ -44,5 +44,5 @@ from ._lib import (  # noqa: F401
     decdec_workspace_bytes,
     decdec_workspace_init,
 )
-from .tp import Comm, P2PLinear, P2PStack, Peers, TPLinear, TPStack, peer_offsets, shard_codes, shard_columns  # noqa: F401
+from .tp import Comm, MLLinear, P2PLinear, P2PStack, Peers, TPLinear, TPStack, peer_offsets, shard_codes, shard_columns  # noqa: F401
 from .layer import HostBuffer, QuantLinear, Stack, Workspace, pack_residual_into, pack_weights, select  # noqa: F401

@@ -80,6 +80,8 @@ def _load():
         "decdec_peers_destroy": (None, [VP]),
         "decdec_linear_p2p": (I32, [Lp, VP, I32, I32, SZ, I32, VP, VP, SZ, VP, VP]),
         "decdec_stack_create_p2p": (I32, [Lp, I32, P(I32), I32, P(VP), P(SZ), VP, SZ, VP, VP, P(VP)]),
+        "decdec_ml_bytes": (SZ, [I32, I32]),
+        "decdec_linear_ml": (I32, [Lp, VP, I32, I32, VP, VP, VP, SZ, VP, SZ, VP]),
     }
     for name, (res, args) in sig.items():
         if os.environ.get("DECDEC_LIB") and not hasattr(lib, name):
@@ -100,7 +102,7 @@ EXPORTED = [
     "decdec_set_dec_ctas", "decdec_nccl_version", "decdec_nccl_unique_id", "decdec_comm_init", "decdec_comm_destroy",
     "decdec_comm_rank", "decdec_comm_nranks", "decdec_linear_tp", "decdec_stack_create_tp",
     "decdec_peers_create", "decdec_peers_connect", "decdec_peers_buffer", "decdec_peers_buffer_bytes",
-    "decdec_peers_destroy", "decdec_linear_p2p", "decdec_stack_create_p2p",
+    "decdec_peers_destroy", "decdec_linear_p2p", "decdec_stack_create_p2p", "decdec_ml_bytes", "decdec_linear_ml",
 ]
 
 
@@ -321,3 +323,12 @@ def decdec_stack_create_p2p(layers, ks, chunk, xs, y_offs, ws, ws_bytes, peers, 
     _check(_lib.decdec_stack_create_p2p(arr, n, karr, chunk, xarr, oarr, _vp(ws), ws_bytes, _vp(peers), _vp(stream),
                                         ctypes.byref(out)), "decdec_stack_create_p2p")
     return int(out.value)
+
+
+def decdec_ml_bytes(d_out: int, nranks: int) -> int:
+    return int(_lib.decdec_ml_bytes(d_out, nranks))
+
+
+def decdec_linear_ml(L: decdec_layer, x, k: int, chunk: int, y, sel, ws, ws_bytes: int, peers, ml_off: int, stream=0):
+    _check(_lib.decdec_linear_ml(ctypes.byref(L), _vp(x), k, chunk, _vp(y), _vp(sel), _vp(ws), ws_bytes, _vp(peers),
+                                 ml_off, _vp(stream)), "decdec_linear_ml")

@@ -364,6 +364,8 @@ decdec_status init_attrs() {
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 16>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4, 3>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4, 4>, lin);
+  if (s == DECDEC_OK) s = set_smem_attr(k_linear<3, 4, 0, 1>, lin);
+  if (s == DECDEC_OK) s = set_smem_attr(k_linear<4, 4, 0, 1>, lin);
   if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<3, 0>, kGemvSmemBudget + 1024);
   if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<4, 0>, kGemvSmemBudget + 1024);
   if (s == DECDEC_OK) s = set_smem_attr(k_gemv16<3, 1>, kGemvSmemBudget + 1024);
@@ -460,7 +462,7 @@ bool coop_launch() {
   return env == 1;
 }
 
-template <int BITS, int RBITS, int LUTB = 0>
+template <int BITS, int RBITS, int LUTB = 0, int MLF = 0>
 decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pl.grid);
@@ -483,11 +485,15 @@ decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, c
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  return cuda_status(cudaLaunchKernelEx(&cfg, k_linear<BITS, RBITS, LUTB>, p));
+  return cuda_status(cudaLaunchKernelEx(&cfg, k_linear<BITS, RBITS, LUTB, MLF>, p));
 }
 
 decdec_status launch_linear(const LinearParams& p, const Plan& pl, int bits, int rbits, bool pdl, cudaStream_t st,
                             int lut_bits = 0) {
+  if (p.share_n > 1) {  // multi-link residual fetch (uniform base, r4 residual)
+    if (lut_bits || rbits != 4) return DECDEC_EUNSUPPORTED;
+    return bits == 3 ? launch_linear_t<3, 4, 0, 1>(p, pl, pdl, st) : launch_linear_t<4, 4, 0, 1>(p, pl, pdl, st);
+  }
   if (lut_bits == 3) return launch_linear_t<4, 4, 3>(p, pl, pdl, st);  // LUT base: W4K nibbles, r4 residual
   if (lut_bits == 4) return launch_linear_t<4, 4, 4>(p, pl, pdl, st);
   if (bits == 3) return rbits == 16 ? launch_linear_t<3, 16>(p, pl, pdl, st) : launch_linear_t<3, 4>(p, pl, pdl, st);
@@ -937,6 +943,48 @@ decdec_status decdec_linear_p2p(const decdec_layer* L, const uint16_t* x, int32_
   if (s != DECDEC_OK) return s;
   if ((s = fill_p2p(&P, L, peers, y_off, slot)) != DECDEC_OK) return s;
   return enqueue_linear(P, (cudaStream_t)stream);
+}
+
+size_t decdec_ml_bytes(int32_t d_out, int32_t nranks) {
+  if (d_out <= 0 || nranks < 1) return 0;
+  return align_up(512 + (size_t)(nranks - 1) * d_out * 4, 256);
+}
+
+decdec_status decdec_linear_ml(const decdec_layer* L, const uint16_t* x, int32_t k, int32_t chunk, uint16_t* y,
+                               int32_t* sel, void* ws, size_t ws_bytes, decdec_peers* peers, size_t ml_off,
+                               decdec_stream_t stream) {
+  if (!L || !peers || peers->nranks < 1) return DECDEC_EINVAL;
+  const int rank = peers->rank, P = peers->nranks;
+  if (ml_off & 15) return DECDEC_EINVAL;
+  if (ml_off + decdec_ml_bytes(L->d_out, P) > peers->user_bytes) return DECDEC_ESPACE;
+  if (P == 1 || rank == 0) {
+    if (!y) return DECDEC_EINVAL;
+  }
+  Prepared Pp;
+  // a helper has no output of its own: its (never written) y is the workspace head
+  decdec_status s = prepare_linear(L, x, k, chunk, rank == 0 ? y : static_cast<uint16_t*>(ws), rank == 0 ? sel : nullptr,
+                                   ws, ws_bytes, &Pp);
+  if (s != DECDEC_OK) return s;
+  if (P == 1 || Pp.gemv || Pp.p.k_sel == 0) {  // nothing to split: the main rank alone, as decdec_linear
+    return rank == 0 ? enqueue_linear(Pp, (cudaStream_t)stream) : DECDEC_OK;
+  }
+  if (Pp.pl.n_dec > 64) return DECDEC_EUNSUPPORTED;  // 64 flag / ack words per layer
+  if (Pp.lut_bits || Pp.rbits != 4) return DECDEC_EUNSUPPORTED;  // built for the uniform base + r4
+  auto user = [&](int q) { return static_cast<uint8_t*>(peers->base[q]) + decdec::kFlagBytes + ml_off; };
+  LinearParams& p = Pp.p;
+  p.share_n = P;
+  p.share_r = rank;
+  if (rank == 0) {
+    p.ml_flag = reinterpret_cast<unsigned int*>(user(0));
+    p.ml_in = reinterpret_cast<const float*>(user(0) + 512);
+    for (int h = 1; h < P; ++h) p.ml_peer_ack[h - 1] = reinterpret_cast<unsigned int*>(user(h) + 256);
+  } else {
+    p.ml_out = reinterpret_cast<float*>(user(0) + 512) + (size_t)(rank - 1) * L->d_out;
+    p.ml_out_flag = reinterpret_cast<unsigned int*>(user(0));
+    p.ml_ack = reinterpret_cast<unsigned int*>(user(rank) + 256);
+    Pp.pl.grid = 0;  // DEC CTAs only: no base GEMV on a helper
+  }
+  return enqueue_linear(Pp, (cudaStream_t)stream);
 }
 
 decdec_status decdec_stack_launch(decdec_stack* g, decdec_stream_t stream) {

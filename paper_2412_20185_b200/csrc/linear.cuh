@@ -97,6 +97,19 @@ struct LinearParams {
   uint16_t* dbg_xs;
   int dbg_cap, dbg_ctas;
   P2PParams pp;  // fused P2P all-gather (p2p.cuh); pp.nranks <= 1: plain local y stores
+  // multi-link residual fetch (NEXT-4, decdec_linear_ml): the DEC CTAs gather only the selected
+  // positions e with e % share_n == share_r.  A helper rank (ml_out) writes its o_dec part
+  // (fp32, x S_j) into the main rank's buffer over NVLink instead of combining; the main rank
+  // (ml_in) adds the helpers' parts in rank order.  Per DEC CTA c: the helper waits until its
+  // ack word c is clear, sets it, writes, and releases one count to the main's flag c; the main
+  // acquires share_n - 1 counts, re-arms its flag, combines, then clears every helper's ack c.
+  int share_n, share_r;
+  float* ml_out;                          // helper: its part buffer in the main rank's region (peer)
+  unsigned int* ml_out_flag;              // helper: the main rank's flags [n_dec] (peer)
+  unsigned int* ml_ack;                   // helper: its own ack words [n_dec]
+  const float* ml_in;                     // main: the helpers' parts [share_n - 1][d_out] (local)
+  unsigned int* ml_flag;                  // main: its flags [n_dec]
+  unsigned int* ml_peer_ack[kMaxPeers];   // main: helper h's ack words (peer), h = 1 .. share_n - 1
 };
 
 // A DEC CTA (steps 1-4 of P:207).  DEC CTA c owns the output segments c, c + n_dec, ...:
@@ -107,7 +120,9 @@ struct LinearParams {
 //   4. after a CTA barrier, a warp per segment waits for the segment's o_b rows (GEMV arrival
 //      count), adds S_j * sum_j part_j in fixed order and writes y.  No global partials, no
 //      value atomics -> deterministic.
-template <int RBITS>
+// MLF = 1: the multi-link residual fetch (NEXT-4) build -- position shares and the helper / main
+// hand-off; MLF = 0 compiles none of it (the single-GPU and tensor-parallel paths)
+template <int RBITS, int MLF = 0>
 __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, int warp, int lane) {
   SelectSmem* S = reinterpret_cast<SelectSmem*>(smem);
   uint4* sx4 = reinterpret_cast<uint4*>(smem + sizeof(SelectSmem));
@@ -156,6 +171,10 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     if (tr) tr[15] = clock64();  // selection phases 16-19 are SM cycles relative to this
   }
   const int n_items = ns * p.gws;
+  // this CTA's share of the selected positions (all of them unless the multi-link fetch splits
+  // them across ranks): local index e -> position share_r + e * share_n
+  const int share_n = MLF ? p.share_n : 1, share_r = MLF ? p.share_r : 0;
+  const int k_local = MLF ? (p.k_sel - share_r + share_n - 1) / share_n : p.k_sel;
   using Vec = typename std::conditional<RBITS == 4, uint32_t, uint4>::type;
   constexpr int kGR = RBITS == 4 ? kGatherRows4 : kGatherRows16;
   // per-warp staging: 2 buffers x kGR rows x 32 lanes x Vec (cp.async destinations)
@@ -164,13 +183,13 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     const int i = it % ns, j = it / ns;
     const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
     const bool cv = col0 < p.d_out;
-    const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
+    const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, k_local);
     Vec* dst = stage + bsel * p.rpi * 32 + lane;
 #pragma unroll
     for (int r = 0; r < kGR; ++r) {
       const int e = e0 + r;
       if (r < p.rpi && e < e1 && cv) {
-        const uint8_t* rowp = p.r_rows + (size_t)sidx[e] * p.r_row_bytes;
+        const uint8_t* rowp = p.r_rows + (size_t)sidx[share_r + e * share_n] * p.r_row_bytes;
         if constexpr (RBITS == 4) cp_async_4(dst + r * 32, rowp + (col0 >> 1));
         else cp_async_16(dst + r * 32, rowp + col0 * 2);
       }
@@ -179,13 +198,13 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   };
   auto consume = [&](int it, int bsel, float* acc) {  // decode + FHFMA into acc[8]
     const int j = it / ns;
-    const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, p.k_sel);
+    const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, k_local);
     const Vec* src = stage + bsel * p.rpi * 32 + lane;
 #pragma unroll
     for (int r = 0; r < kGR; ++r) {
       const int e = e0 + r;
       if (r < p.rpi && e < e1) {
-        const uint16_t xv = sxs[e];
+        const uint16_t xv = sxs[share_r + e * share_n];
         const Vec w = src[r * 32];
         uint32_t cq[4];
         if constexpr (RBITS == 4) {
@@ -255,8 +274,8 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     nD = p.k_sel;
   }
   bool rest_seen = nD >= p.k_sel;
-  auto ready = [&](int item) {  // the rows of `item` are placed
-    if (!rest_seen && min((item / ns) * p.rpi + p.rpi, p.k_sel) > nD) {
+  auto ready = [&](int item) {  // the rows of `item` are placed (its last position is < nD)
+    if (!rest_seen && share_r + (min((item / ns) * p.rpi + p.rpi, k_local) - 1) * share_n >= nD) {
       select_wait_rest(SS);
       rest_seen = true;
     }
@@ -302,6 +321,57 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   if (RBITS == 4 && warp < ns) mbar_wait(scale_bar, 0);  // the scales' bulk copies landed
   if (tr && threadIdx.x == 0) tr[4] = clock64();
   if (threadIdx.x == 0) DECDEC_TRACE(p, 12);
+  if (MLF && p.ml_out) {  // multi-link helper: this rank's o_dec part -> the main rank, no combine
+    if (threadIdx.x == 0) {  // the main rank has consumed this CTA's previous part
+      const unsigned long long t0 = globaltimer();
+      while (ld_acquire_sys_u32(p.ml_ack + blockIdx.x) != 0u) {
+        __nanosleep(64);
+        if (globaltimer() - t0 > 20000000000ull) __trap();
+      }
+      p.ml_ack[blockIdx.x] = 1u;
+    }
+    __syncthreads();
+    for (int i = warp; i < ns; i += nw) {
+      const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
+      if (col0 < p.d_out) {
+        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j < p.nparts; ++j) {  // fixed order: slots ascending
+          const float* pp = spart + ((size_t)i * p.nparts + j) * kSegCols + lane * 8;
+          const float4 a = *reinterpret_cast<const float4*>(pp), b = *reinterpret_cast<const float4*>(pp + 4);
+          v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+          v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+        }
+        if (RBITS == 4) {
+          const uint4 sv = *reinterpret_cast<const uint4*>(srsc + i * kSegCols + lane * 8);
+          const uint32_t sw[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            v[2 * e] *= __half2float(__ushort_as_half((unsigned short)(sw[e] & 0xffffu)));
+            v[2 * e + 1] *= __half2float(__ushort_as_half((unsigned short)(sw[e] >> 16)));
+          }
+        }
+        *reinterpret_cast<float4*>(p.ml_out + col0) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(p.ml_out + col0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.ml_out_flag + blockIdx.x) : "memory");
+    }
+    return;
+  }
+  if (MLF && p.ml_in) {  // multi-link main: every helper's part of this CTA's segments has landed
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = globaltimer();
+      while (ld_acquire_sys_u32(p.ml_flag + blockIdx.x) < (unsigned)(p.share_n - 1)) {
+        __nanosleep(64);
+        if (globaltimer() - t0 > 20000000000ull) __trap();
+      }
+      p.ml_flag[blockIdx.x] = 0u;  // re-armed: no helper writes again before its ack is cleared
+    }
+    __syncthreads();
+  }
   // ---- step 4: combine, one warp per local segment.  o_b entries are self-validating (relaxed
   // stores of the GEMV CTAs, kObEmpty until written): poll them, then restore kObEmpty.
   for (int i = warp; i < ns; i += nw) {
@@ -340,11 +410,29 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
       const float o[8] = {__uint_as_float(o0.x), __uint_as_float(o0.y), __uint_as_float(o0.z), __uint_as_float(o0.w),
                           __uint_as_float(o1.x), __uint_as_float(o1.y), __uint_as_float(o1.z), __uint_as_float(o1.w)};
       uint32_t out[4];
+      if (MLF && p.ml_in) {  // own part x S_j, then the helpers' parts in rank order, then + o_b
+        float d[8];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const __half lo = __float2half_rn(fmaf(Sc[2 * e], sum[2 * e], o[2 * e]));
-        const __half hi = __float2half_rn(fmaf(Sc[2 * e + 1], sum[2 * e + 1], o[2 * e + 1]));
-        out[e] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+        for (int e = 0; e < 8; ++e) d[e] = Sc[e] * sum[e];
+        for (int h = 0; h < p.share_n - 1; ++h) {
+          const float* hp = p.ml_in + (size_t)h * p.d_out + col0;
+          const float4 a = ld_relaxed_sys_f4(hp), b = ld_relaxed_sys_f4(hp + 4);
+          d[0] += a.x; d[1] += a.y; d[2] += a.z; d[3] += a.w;
+          d[4] += b.x; d[5] += b.y; d[6] += b.z; d[7] += b.w;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const __half lo = __float2half_rn(o[2 * e] + d[2 * e]);
+          const __half hi = __float2half_rn(o[2 * e + 1] + d[2 * e + 1]);
+          out[e] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const __half lo = __float2half_rn(fmaf(Sc[2 * e], sum[2 * e], o[2 * e]));
+          const __half hi = __float2half_rn(fmaf(Sc[2 * e + 1], sum[2 * e + 1], o[2 * e + 1]));
+          out[e] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+        }
       }
       p2p_store_u4(p.pp, p.y, col0, make_uint4(out[0], out[1], out[2], out[3]));
       const uint4 empty = make_uint4(kObEmpty, kObEmpty, kObEmpty, kObEmpty);
@@ -353,6 +441,14 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     }
   }
   if (threadIdx.x == 0) DECDEC_TRACE(p, 9);
+  if (MLF && p.ml_in) {  // the helpers' parts are consumed: let them write the next ones
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int h = 0; h < p.share_n - 1; ++h)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.ml_peer_ack[h] + blockIdx.x), "r"(0u) : "memory");
+    }
+  }
   if (p.pp.nranks > 1) {  // fused all-gather: this CTA's segments are in every rank's y_full
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -374,7 +470,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
 // LUTB = 0: uniform base (W3K / W4K codes, per-group fp16 scale + u8 zero); LUTB = 3 | 4: the
 // non-uniform base (NEXT-3, P:397 / P:502): W4K nibble codes (BITS = 4) and, in place of the
 // scales, each row's table of 2^LUTB fp16 values; no zeros.
-template <int BITS, int RBITS, int LUTB = 0>
+template <int BITS, int RBITS, int LUTB = 0, int MLF = 0>
 __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stage0 = smem;
@@ -397,7 +493,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
 
   // ------------------------------------------------------------------ DEC CTAs (steps 1-4)
   if ((int)blockIdx.x < p.n_dec) {
-    dec_cta<RBITS>(p, smem, warp, lane);
+    dec_cta<RBITS, MLF>(p, smem, warp, lane);
     return;
   }
   const int cta = blockIdx.x - p.n_dec, n_cta = gridDim.x - p.n_dec;  // GEMV CTA index / count

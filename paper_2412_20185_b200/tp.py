@@ -241,3 +241,36 @@ class P2PStack:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------ multi-link residual fetch
+class MLLinear:
+    """NEXT-4 multi-link residual fetch (decdec_linear_ml): every rank of the peer group holds the
+    FULL layer (its own host-mapped copy of the residual; base weights used on rank 0 only) and is
+    called with the same x / k.  Rank r gathers the selected positions p with p % world == r over
+    its own PCIe link; helpers (r > 0) store their o_dec parts into rank 0's user area at ml_off
+    (decdec_ml_bytes) over NVLink; rank 0 writes y.  Returns y on rank 0, None on helpers."""
+
+    def __init__(self, linear, peers: Peers, ml_off: int):
+        self.lin, self.peers, self.ml_off = linear, peers, int(ml_off)
+
+    @staticmethod
+    def area_bytes(d_out: int, world: int) -> int:
+        from paper_2412_20185_b200 import _lib
+
+        return _lib.decdec_ml_bytes(d_out, world)
+
+    def __call__(self, x, k: int, chunk: int = 0, y=None, sel=None, workspace=None, stream=None):
+        import torch
+        from paper_2412_20185_b200 import _lib
+        from paper_2412_20185_b200.layer import Workspace, _stream_ptr
+
+        main = self.peers.rank == 0
+        if main and y is None:
+            y = torch.empty(self.lin.d_out, dtype=torch.float16, device=x.device)
+        if workspace is None:
+            workspace = Workspace(max(k, 1), self.lin.d_out)
+        _lib.decdec_linear_ml(self.lin.struct, x.data_ptr(), k, chunk, y.data_ptr() if main else 0,
+                              sel.data_ptr() if (sel is not None and main) else 0, workspace.ptr, workspace.nbytes,
+                              self.peers.handle, self.ml_off, _stream_ptr(stream))
+        return y if main else None

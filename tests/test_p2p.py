@@ -136,3 +136,91 @@ def test_bench_two_ranks_fused_allgather_path():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and "p2p" in line["config"]["parallelism"], line["config"]
     assert set(line["sweep"]) == {"0", "21"}
+
+
+# ------------------------------------------------------------------ NEXT-4: multi-link residual fetch
+ML_CASES = [(1024, 1024, 16), (4096, 4096, 84), (4096, 28672, 84), (14336, 4096, 294), (4096, 4096, 0)]
+
+
+def _ml_worker(rank, world, port, out_dir, multi_gpu):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    import paper_2412_20185_b200 as dd
+    from synth import gen_activations, gen_perf_layer, layer_seed
+
+    torch.cuda.set_device(rank if multi_gpu else 0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    offs, o = [], 0
+    for _, d_out, _ in ML_CASES:
+        offs.append(o)
+        o += dd.MLLinear.area_bytes(d_out, world)
+    peers = dd.Peers(o)
+    out = {}
+    try:
+        for i, (d_in, d_out, k) in enumerate(ML_CASES):
+            L = gen_perf_layer(d_in, d_out, 3, seed=layer_seed("ml", d_in, d_out))  # every rank: the full layer
+            lin = dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"])
+            ml = dd.MLLinear(lin, peers, offs[i])
+            ws = dd.Workspace(max(k, 1), d_out)
+            for rep in range(3):  # the same ml area again and again: the flag / ack handshake
+                x = gen_activations(d_in, 1, seed=layer_seed("ml", "x", i, rep), kind="d" if d_in > 8192 else "qkv")[0]
+                sel = torch.empty(max(k, 1), dtype=torch.int32, device="cuda")
+                y = ml(torch.from_numpy(x).cuda(), k, sel=sel, workspace=ws)
+                torch.cuda.synchronize()
+                if rank == 0:
+                    out[f"y{i}_{rep}"] = y.cpu().numpy()
+                    out[f"s{i}_{rep}"] = sel.cpu().numpy()[:k]
+        dist.barrier()
+        if rank == 0:
+            np.savez(os.path.join(out_dir, "ml_rank0.npz"), **out)
+    finally:
+        peers.close()
+        dist.destroy_process_group()
+
+
+def _run_ml(tmp_path, multi_gpu):
+    import time
+
+    import torch.multiprocessing as mp
+
+    import oracle
+    from synth import gen_activations, gen_perf_layer, layer_seed
+
+    world = 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.start_processes(_ml_worker, args=(world, port, str(tmp_path), multi_gpu), nprocs=world, join=False,
+                             start_method="spawn")
+    t0 = time.time()
+    while not ctx.join(timeout=5):
+        if time.time() - t0 > 600:
+            for p in ctx.processes:
+                p.kill()
+            raise AssertionError("multi-link ranks did not finish in 600 s")
+    out = np.load(os.path.join(tmp_path, "ml_rank0.npz"))
+    for i, (d_in, d_out, k) in enumerate(ML_CASES):
+        L = gen_perf_layer(d_in, d_out, 3, seed=layer_seed("ml", d_in, d_out))
+        W_hat = oracle.dequantize_base(L["q"], L["s"], L["z"])
+        for rep in range(3):
+            x = gen_activations(d_in, 1, seed=layer_seed("ml", "x", i, rep), kind="d" if d_in > 8192 else "qkv")[0]
+            ref = oracle.decdec_linear_ref(L["q"], L["s"], L["z"], x, k, rc=L["rc"], rS=L["rS"], W_hat=W_hat)
+            if k:
+                assert np.array_equal(out[f"s{i}_{rep}"], ref["idx"]), (i, rep)
+            ok, err, bound = oracle.tolerance_ok(out[f"y{i}_{rep}"], ref["y64"], ref["A"])
+            assert ok.all(), (i, rep, int((~ok).sum()))
+
+
+def test_multilink_fetch_two_ranks_same_gpu(tmp_path):
+    """NEXT-4: rank 1 gathers every other selected row over its own link and hands its o_dec part
+    to rank 0 (here both share GPU 0 and its link); rank 0's y must equal the UNSHARDED oracle
+    (all k rows) within L9, with the exact selection, over repeated calls on one ml area."""
+    _run_ml(tmp_path, multi_gpu=False)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multilink_fetch_two_gpus(tmp_path):
+    _run_ml(tmp_path, multi_gpu=True)
