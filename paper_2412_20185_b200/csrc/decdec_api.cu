@@ -478,7 +478,7 @@ decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, c
   }
   // cooperative: DEC CTAs wait for GEMV CTAs of the same grid; the fused P2P all-gather's
   // leader waits for the other CTAs' signals
-  if ((p.k_sel > 0 && coop_launch()) || p.pp.nranks > 1) {
+  if ((p.k_sel > 0 && coop_launch()) || p.pp.active) {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na].val.cooperative = 1;
     ++na;
@@ -779,6 +779,7 @@ decdec_status check_p2p(const decdec_layer* L, const decdec_peers* pe, size_t y_
 decdec_status fill_p2p(Prepared* P, const decdec_layer* L, const decdec_peers* pe, size_t y_off, int slot) {
   if (P->gemv) return DECDEC_EUNSUPPORTED;  // LUT base / DECDEC_NEW_GEMV: k_gemv16 has no exchange epilogue
   decdec::P2PParams& pp = P->p.pp;
+  pp.active = 1;
   pp.nranks = pe->nranks;
   pp.n_writers = P->p.k_sel > 0 ? P->pl.n_dec : P->pl.grid;  // DEC CTAs (combine) or GEMV CTAs write y
   pp.leader = 0;
@@ -787,6 +788,7 @@ decdec_status fill_p2p(Prepared* P, const decdec_layer* L, const decdec_peers* p
     pp.peer_flag[q] = static_cast<unsigned int*>(pe->base[q]) + (size_t)slot * decdec::kFlagStrideWords;
   }
   pp.my_flag = pp.peer_flag[pe->rank];
+  pp.my_count = pp.my_flag + 1;
   return DECDEC_OK;
 }
 

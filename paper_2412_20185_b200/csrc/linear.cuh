@@ -449,7 +449,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.ml_peer_ack[h] + blockIdx.x), "r"(0u) : "memory");
     }
   }
-  if (p.pp.nranks > 1) {  // fused all-gather: this CTA's segments are in every rank's y_full
+  if (p.pp.active) {  // fused all-gather: this CTA's segments are in every rank's y_full
     __syncthreads();
     if (threadIdx.x == 0) {
       p2p_signal(p.pp);
@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     }
     if (ct == 0) DECDEC_TRACE(p, 4);
     if (ct == 0) DECDEC_TRACE(p, 10);  // last o_b row stored (this warp)
-    if (p.k_sel == 0 && p.pp.nranks > 1) {  // fused all-gather (k = 0: the GEMV CTAs write y)
+    if (p.k_sel == 0 && p.pp.active) {  // fused all-gather (k = 0: the GEMV CTAs write y)
       named_bar_sync(15, p.NC * 32);
       if (ct == 0) {
         p2p_signal(p.pp);
