@@ -445,68 +445,6 @@ __device__ __forceinline__ void select_wait_rest(const SelectSmemS* S) {
   __threadfence_block();
 }
 
-// Finisher (one warp): sort the threshold-bin candidates (index << 15 | key) by index with a
-// warp bitonic network over 32*E slots (E per lane, slot = lane + 32 h), then write the taken
-// ones (key > T, or key == T among the first `need` ties) at positions nD.. in index order.
-template <int E>
-__device__ __forceinline__ void select_finish_list(const SelectSmemS* SS, const uint16_t* __restrict__ x, uint32_t ncand,
-                                                   uint32_t T, uint32_t need, uint32_t nD, int* __restrict__ idx_out,
-                                                   uint16_t* __restrict__ xs_out) {
-  const int lane = threadIdx.x & 31;
-  constexpr int N = 32 * E;
-  uint32_t e[E];
-#pragma unroll
-  for (int h = 0; h < E; ++h) e[h] = (uint32_t)(lane + 32 * h) < ncand ? SS->cand[lane + 32 * h] : 0xffffffffu;
-#pragma unroll
-  for (int k2 = 2; k2 <= N; k2 <<= 1) {
-#pragma unroll
-    for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-      if (j2 >= 32) {  // partner in the same lane: slot h ^ (j2 / 32)
-        const int jh = j2 >> 5;
-#pragma unroll
-        for (int h = 0; h < E; ++h) {
-          if (h & jh) continue;
-          const int pos = lane + 32 * h;
-          const bool up = (pos & k2) == 0;
-          const uint32_t lo = min(e[h], e[h | jh]), hi = max(e[h], e[h | jh]);
-          e[h] = up ? lo : hi;
-          e[h | jh] = up ? hi : lo;
-        }
-      } else {
-#pragma unroll
-        for (int h = 0; h < E; ++h) {
-          const int pos = lane + 32 * h;
-          const uint32_t o = __shfl_xor_sync(0xffffffffu, e[h], j2);
-          const bool up = (pos & k2) == 0;
-          const bool lower = (pos & j2) == 0;
-          e[h] = (lower == up) ? min(e[h], o) : max(e[h], o);
-        }
-      }
-    }
-  }
-  // slots are now in index order along (h, lane)
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t taken_before = 0, eq_before = 0;
-#pragma unroll
-  for (int h = 0; h < E; ++h) {
-    const uint32_t v = e[h];
-    const bool valid = v != 0xffffffffu;
-    const uint32_t key = v & 0x7fffu;
-    const bool gt = valid && key > T, eq = valid && key == T;
-    const uint32_t beq = __ballot_sync(0xffffffffu, eq);
-    const uint32_t my_eq = eq_before + __popc(beq & lt);
-    const bool take = gt || (eq && my_eq < need);
-    const uint32_t bt = __ballot_sync(0xffffffffu, take);
-    if (take) {
-      const uint32_t pos = nD + taken_before + __popc(bt & lt);
-      idx_out[pos] = (int)(v >> 15);
-      xs_out[pos] = x[v >> 15];
-    }
-    taken_before += __popc(bt);
-    eq_before += __popc(beq);
-  }
-}
-
 template <int MAXC>
 __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int n, int q, int* __restrict__ idx_out,
                                             uint16_t* __restrict__ xs_out, int* __restrict__ sel_out, SelectSmemS* SS,
