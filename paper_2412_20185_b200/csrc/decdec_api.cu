@@ -478,7 +478,7 @@ decdec_status launch_linear_t(const LinearParams& p, const Plan& pl, bool pdl, c
   }
   // cooperative: DEC CTAs wait for GEMV CTAs of the same grid; the fused P2P all-gather's
   // leader waits for the other CTAs' signals
-  if ((p.k_sel > 0 && coop_launch()) || p.pp.active) {
+  if ((p.k_sel > 0 && coop_launch()) || (p.pp.active && p.pp.wait_self)) {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na].val.cooperative = 1;
     ++na;
@@ -783,12 +783,13 @@ decdec_status fill_p2p(Prepared* P, const decdec_layer* L, const decdec_peers* p
   pp.nranks = pe->nranks;
   pp.n_writers = P->p.k_sel > 0 ? P->pl.n_dec : P->pl.grid;  // DEC CTAs (combine) or GEMV CTAs write y
   pp.leader = 0;
+  pp.wait_self = 1;  // standalone call: returns with y_full complete (stacks defer all but the last)
+  pp.prev_flag = nullptr;
   for (int q = 0; q < pe->nranks; ++q) {
     pp.peer_y[q] = p2p_shard(pe, q, y_off, L->d_out);
     pp.peer_flag[q] = static_cast<unsigned int*>(pe->base[q]) + (size_t)slot * decdec::kFlagStrideWords;
   }
   pp.my_flag = pp.peer_flag[pe->rank];
-  pp.my_count = pp.my_flag + 1;
   return DECDEC_OK;
 }
 
@@ -836,6 +837,11 @@ decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const i
         s = prepare_linear(&layers[i], x[i], k[i], chunk, p2p_shard(peers, peers->rank, y_off[i], layers[i].d_out),
                            nullptr, ws, ws_bytes, &P[i]);
       if (s == DECDEC_OK) s = fill_p2p(&P[i], &layers[i], peers, y_off[i], i);
+      if (s == DECDEC_OK) {  // only the last layer returns with its y_full complete; layer i > 0
+        decdec::P2PParams& pp = P[i].p.pp;  // first waits for layer i - 1's (deferred wait)
+        pp.wait_self = i == n_layers - 1;
+        if (i > 0) pp.prev_flag = static_cast<unsigned int*>(peers->base[peers->rank]) + (size_t)(i - 1) * decdec::kFlagStrideWords;
+      }
     } else {
       uint16_t* yi = y[i] ? y[i] + (size_t)rank * layers[i].d_out : nullptr;
       s = prepare_linear(&layers[i], x[i], k[i], chunk, yi, nullptr, ws, ws_bytes, &P[i]);

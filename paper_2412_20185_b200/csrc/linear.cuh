@@ -166,6 +166,10 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   }
   __syncthreads();
   pdl_wait();  // x may be the previous layer's product; the workspace is the previous layer's
+  if (p.pp.prev_flag) {  // TP stack: the previous layer's y_full is complete on every rank
+    if (threadIdx.x == 0) p2p_wait_prev(p.pp);
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     DECDEC_TRACE(p, 5);
     if (tr) tr[15] = clock64();  // selection phases 16-19 are SM cycles relative to this
@@ -453,7 +457,6 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     __syncthreads();
     if (threadIdx.x == 0) {
       p2p_signal(p.pp);
-      if ((int)blockIdx.x == p.pp.leader) p2p_wait_all(p.pp);
     }
   }
   if (p.dbg_idx && (int)blockIdx.x < p.dbg_ctas) {  // every DEC CTA's own selection, for tests
@@ -555,6 +558,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
     const int rot = (BITS == 4) ? ((g >> 1) & 3) : 0;  // 4-bit: bank-conflict-free 16-B chunk order
     // x (and the workspace) belong to the previous layer until it completes
     pdl_wait();
+    if (p.pp.prev_flag) {  // TP stack: the previous layer's y_full is complete on every rank
+      if (ct == 0) p2p_wait_prev(p.pp);
+      named_bar_sync(12, p.NC * 32);
+    }
     if (ct == 0) DECDEC_TRACE(p, 8);
     // Stage x in smem first: a lane owns 256 contiguous bytes of x, so loading its registers
     // straight from global memory touches 32 cache lines per instruction and the L1 serialises
@@ -821,7 +828,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_linear(const LinearParams p)
       named_bar_sync(15, p.NC * 32);
       if (ct == 0) {
         p2p_signal(p.pp);
-        if ((int)blockIdx.x == p.pp.leader) p2p_wait_all(p.pp);
       }
     }
     return;
