@@ -107,7 +107,8 @@ def gen_perf_layer_device(d_in: int, d_out: int, bits: int, seed: int, device="c
     """Perf-harness layer drawn directly on the GPU (torch RNG, seeded): uniformly random
     packed code bits (every layout here is a bijection between code bits and words, so
     random words == iid uniform codes), scales/zeros per the §8(d) recipe, and random
-    residual row bytes (nibbles uniform on [0, 15]) plus residual scales.
+    residual row bytes (nibbles uniform on [1, 15], i.e. residual codes c = n - 8 on [-7, 7],
+    the domain of Q_r) plus residual scales.
     Returns device tensors: w uint8 [d_out * d_in * bits / 8], s fp16 [d_out * G],
     z uint8 [d_out * G], r uint8 [d_in * d_out / 2], rS fp16 [d_out]."""
     import torch
