@@ -44,6 +44,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 struct Plan {
   int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, n_dec;  // grid = GEMV CTAs (+ n_dec DEC CTAs)
   int n_seg, rpi, gws, nparts, one_seg;  // DEC: output segments, rows per gather item, items and partials per segment
+  int early_reads;                       // DEC: read the D rows during the selection (linear.cuh)
   uint32_t stage_bytes, off_s, off_z, off_sel, off_x, off_part, off_rsc, off_stage;
   size_t smem;
 };
@@ -74,6 +75,20 @@ int dec_ctas(int warps_per_cta, double r) {
   const int base = r < 1.0 ? 272 : (r < 2.5 ? 544 : 1088);  // gather warps
   int n = (base + warps_per_cta - 1) / warps_per_cta;
   return n < 2 ? 2 : (n > 64 ? 64 : n);
+}
+
+// Early D-row reads (linear.cuh dec_cta): on for calls whose PCIe/HBM roofline ratio r lies in
+// [kEarlyLo, kEarlyHi] -- measured on the Llama-3-8B step (1x B200, same box A/B): k_chunk 21
+// (r ~3.4) -3.6 %, k_chunk 8 (r ~1.3) +-0, k_chunk 1-4 (r < 0.7) +2-3 %, k_chunk 32 (r ~5.2)
+// +0.6 %.  DECDEC_EARLY=0|1 forces it.
+int early_reads(double r) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("DECDEC_EARLY");
+    env = e ? atoi(e) : -1;
+  }
+  if (env >= 0) return env > 0;
+  return r >= 1.5 && r <= 4.5;
 }
 
 // DEC CTA layout: CTA c owns segments c, c + n_dec, ...; a segment's k_sel rows are split in
@@ -199,6 +214,7 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
       p.n_dec = 0;
       if (k_sel > 0 && !plan_dec(d_out, k_sel, sel_len, 1 + nc, r_bits == 16 ? kGatherRows16 : kGatherRows4, r_ratio, &p))
         continue;
+      p.early_reads = k_sel > 0 && early_reads(r_ratio);
       const int max_grid = sms - p.n_dec;
       if (max_grid <= 0) continue;
       p.grid = p.n_tiles < max_grid ? p.n_tiles : max_grid;
@@ -750,6 +766,7 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
     p.gws = P.pl.gws;
     p.nparts = P.pl.nparts;
     p.one_seg = P.pl.one_seg;
+    p.early_reads = P.pl.early_reads;
   }
   *out = P;
   return DECDEC_OK;

@@ -87,6 +87,7 @@ struct LinearParams {
   // deterministic result in every DEC CTA, no cross-CTA hand-off), keeps S and x[S] in smem and
   // gathers its share of the (segment, row chunk) items.  The other CTAs run the GEMV.
   int n_dec, k_req, chunk;
+  int early_reads;  // read the D rows' bytes during the selection (plan: PCIe/HBM ratio window)
   int prefetch;  // weight tiles requested per CTA (into smem) before griddepcontrol.wait
   int l2pf;      // further tiles per CTA prefetched into L2 only before griddepcontrol.wait
   int x_pf;      // prefetch x into L2 before griddepcontrol.wait
@@ -242,7 +243,31 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   bool issued = false;
   if (split) {
 #ifndef DECDEC_SPLIT_BARRIER
-    nD = select_split_any(p.x, p.d_in, p.k_req, sidx, sxs, blockIdx.x == 0 ? p.sel_out : nullptr, SS, nw - 1, tr);
+    {
+      // D rows are known before barrier 2: when the plan asks for it (p.early_reads), this CTA
+      // reads their bytes of all its segments right away -- cp.async.ca into a scratch slot, so
+      // the lines land in this SM's L1 and the gather that follows hits them.  Measured (1x B200,
+      // Llama-3-8B step): k_chunk 21 -3.6 %, k_chunk 1-4 +2-3 % (the reads delay the selection's
+      // last phases while few rows profit), hence a window on the call's PCIe/HBM ratio.
+      struct Early {
+        const LinearParams* pp;
+        Vec* dummy;
+        int ns, lane;
+        __device__ __forceinline__ bool on() const { return pp->early_reads != 0; }
+        __device__ __forceinline__ void operator()(int row) const {
+          const uint8_t* rowp = pp->r_rows + (size_t)row * pp->r_row_bytes;
+          for (int i = 0; i < ns; ++i) {
+            const int col0 = ((int)blockIdx.x + i * pp->n_dec) * kSegCols + lane * 8;
+            if (col0 < pp->d_out) {
+              if constexpr (RBITS == 4) cp_async_4(dummy, rowp + (col0 >> 1));
+              else cp_async_16(dummy, rowp + col0 * 2);
+            }
+          }
+        }
+      } early{&p, reinterpret_cast<Vec*>(SS->scratch) + lane, ns, lane};
+      nD = select_split_any(p.x, p.d_in, p.k_req, sidx, sxs, blockIdx.x == 0 ? p.sel_out : nullptr, SS, nw - 1, tr, early);
+      if (p.early_reads) cp_async_commit();
+    }
 #else
     auto early = [&](int n_def) {  // cp.async only: the remaining block barriers do not wait for it
       if (it < n_items && min((it / ns) * p.rpi + p.rpi, p.k_sel) <= n_def) {
@@ -309,6 +334,7 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     consume(it, b, acc);
     if (!one_seg) store_part(it % ns, it / ns, acc);
   }
+  cp_async_wait<0>();  // no cp.async (gather or early read) outstanding past this point
   if (one_seg && had_item) store_part(0, warp, acc);
   if (lane == 0 && (warp == 0 || warp == nw - 1)) DECDEC_TRACE(p, warp == 0 ? 7 : 1);  // gather done
   // the combine warp of local segment `warp` reads its o_b entries before the barrier: the GEMV

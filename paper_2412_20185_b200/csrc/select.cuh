@@ -426,6 +426,7 @@ struct SelectSmemS {
   uint32_t cand[kCandList];  // (index << 15 | key) of threshold-bin candidates: warp w's, in index
                              // order, at [w * cap, w * cap + wcand[w]), cap = kCandList / warps
   uint32_t wcand[kSelMaxWarps];  // candidates per warp (written by each warp's lane 31)
+  uint32_t scratch[128];         // never read: destination of the DEC CTA's early D-row reads
   uint32_t rest_ready;
   uint32_t ncand;
   uint32_t pad[2];
@@ -445,10 +446,14 @@ __device__ __forceinline__ void select_wait_rest(const SelectSmemS* S) {
   __threadfence_block();
 }
 
-template <int MAXC>
+struct NoEarly {
+  __device__ __forceinline__ bool on() const { return false; }
+  __device__ __forceinline__ void operator()(int) const {}
+};
+template <int MAXC, typename Early = NoEarly>
 __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int n, int q, int* __restrict__ idx_out,
                                             uint16_t* __restrict__ xs_out, int* __restrict__ sel_out, SelectSmemS* SS,
-                                            int finisher, unsigned long long* tr) {
+                                            int finisher, unsigned long long* tr, Early early = Early()) {
 #define SEL_TRACE(i)                                  \
   do {                                                \
     if (tr && threadIdx.x == 0) tr[i] = clock64();     \
@@ -542,6 +547,25 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
       }
     }
   }
+#ifndef DECDEC_NO_EARLY
+  // every D key of the warp handed to `early` warp-collectively before barrier 2 (the caller
+  // starts fetching those rows while the rest of the selection runs)
+  if (early.on())
+  for (int m = 0; m < MAXC; ++m) {
+    uint32_t any = __ballot_sync(0xffffffffu, dmask[m] != 0u);
+    while (any) {
+      const int src = __ffs(any) - 1;
+      any &= any - 1;
+      uint32_t bits = __shfl_sync(0xffffffffu, dmask[m], src);
+      const int base = 8 * (__shfl_sync(0xffffffffu, c0, src) + m);
+      while (bits) {
+        const int jj = __ffs(bits) - 1;
+        bits &= bits - 1;
+        early(base + jj);
+      }
+    }
+  }
+#endif
   if (lane == 31) S->wsum[wid] = inc_d;
   __syncthreads();  // barrier 2: histB, bitmap, D warp totals complete
   uint32_t pre_d;
@@ -713,14 +737,16 @@ __device__ __forceinline__ bool select_block_regs_any(const uint16_t* x, int n, 
 }
 
 // Returns D (>= 0), or -1 if the segment does not fit in registers (caller falls back).
+template <typename Early = NoEarly>
 __device__ __forceinline__ int select_split_any(const uint16_t* x, int n, int q, int* idx_out, uint16_t* xs_out,
-                                                int* sel_out, SelectSmemS* S, int finisher, unsigned long long* tr) {
+                                                int* sel_out, SelectSmemS* S, int finisher, unsigned long long* tr,
+                                                Early early = Early()) {
   const int C = ((n >> 3) + (int)blockDim.x - 1) / (int)blockDim.x;
   if (n > 32 * 1024) return -1;
-  if (C <= 1) return select_split<1>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
-  if (C <= 2) return select_split<2>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
-  if (C <= 4) return select_split<4>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
-  if (C <= 8) return select_split<8>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr);
+  if (C <= 1) return select_split<1>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr, early);
+  if (C <= 2) return select_split<2>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr, early);
+  if (C <= 4) return select_split<4>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr, early);
+  if (C <= 8) return select_split<8>(x, n, q, idx_out, xs_out, sel_out, S, finisher, tr, early);
   return -1;
 }
 
