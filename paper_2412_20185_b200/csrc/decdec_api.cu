@@ -44,7 +44,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 struct Plan {
   int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, n_dec;  // grid = GEMV CTAs (+ n_dec DEC CTAs)
   int n_seg, rpi, gws, nparts, one_seg;  // DEC: output segments, rows per gather item, items and partials per segment
-  int early_reads;                       // DEC: read the D rows during the selection (linear.cuh)
+  int early_reads, early_cap;            // DEC: read the D rows during the selection (linear.cuh)
   uint32_t stage_bytes, off_s, off_z, off_sel, off_x, off_part, off_rsc, off_stage;
   size_t smem;
 };
@@ -81,6 +81,23 @@ int dec_ctas(int warps_per_cta, double r) {
 // [kEarlyLo, kEarlyHi] -- measured on the Llama-3-8B step (1x B200, same box A/B): k_chunk 21
 // (r ~3.4) -3.6 %, k_chunk 8 (r ~1.3) +-0, k_chunk 1-4 (r < 0.7) +2-3 %, k_chunk 32 (r ~5.2)
 // +0.6 %.  DECDEC_EARLY=0|1 forces it.
+// Early reads per warp at most (DECDEC_EARLY_CAP, 0 = every D row the warp holds): an SM keeps
+// few zero-copy requests in flight, so a warp with many D rows stalls in its early-read loop and
+// holds up the selection's barrier 2 (d layer: D placed at ~19000 instead of ~12000 cycles).
+// Measured (1x B200, Llama-3-8B k_chunk-21 step, 4 alternating runs): cap 4 -1.6 % vs no cap with
+// the 4-B gather, +-0 with the 16-B gather (profiles/r02_s3_experiments.json).
+int early_cap() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DECDEC_EARLY_CAP");
+    env = e ? atoi(e) : 4;
+    if (env < 0) env = 0;
+    const char* f = getenv("DECDEC_EARLY_SPARE_FIN");  // 1: the finisher warp issues none
+    if (f && atoi(f) > 0) env |= 1 << 16;
+  }
+  return env;
+}
+
 int early_reads(double r) {
   static int env = -2;
   if (env == -2) {
@@ -215,6 +232,7 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
       if (k_sel > 0 && !plan_dec(d_out, k_sel, sel_len, 1 + nc, r_bits == 16 ? kGatherRows16 : kGatherRows4, r_ratio, &p))
         continue;
       p.early_reads = k_sel > 0 && early_reads(r_ratio);
+      p.early_cap = early_cap();
       const int max_grid = sms - p.n_dec;
       if (max_grid <= 0) continue;
       p.grid = p.n_tiles < max_grid ? p.n_tiles : max_grid;
@@ -767,6 +785,7 @@ decdec_status prepare_linear(const decdec_layer* L, const uint16_t* x, int32_t k
     p.nparts = P.pl.nparts;
     p.one_seg = P.pl.one_seg;
     p.early_reads = P.pl.early_reads;
+    p.early_cap = P.pl.early_cap;
   }
   *out = P;
   return DECDEC_OK;

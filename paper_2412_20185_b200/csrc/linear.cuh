@@ -88,6 +88,7 @@ struct LinearParams {
   // gathers its share of the (segment, row chunk) items.  The other CTAs run the GEMV.
   int n_dec, k_req, chunk;
   int early_reads;  // read the D rows' bytes during the selection (plan: PCIe/HBM ratio window)
+  int early_cap;    // ... at most this many rows per warp (0 = all)
   int prefetch;  // weight tiles requested per CTA (into smem) before griddepcontrol.wait
   int l2pf;      // further tiles per CTA prefetched into L2 only before griddepcontrol.wait
   int x_pf;      // prefetch x into L2 before griddepcontrol.wait
@@ -184,8 +185,36 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   constexpr int kGR = RBITS == 4 ? kGatherRows4 : kGatherRows16;
   // per-warp staging: 2 buffers x kGR rows x 32 lanes x Vec (cp.async destinations)
   Vec* stage = reinterpret_cast<Vec*>(smem + p.off_stage) + (size_t)warp * 2 * p.rpi * 32;
+#ifndef DECDEC_NARROW_GATHER
+  // 4-bit R, wide gather: ONE 16-B cp.async per lane covers 4 rows x the segment's 128 B (lanes
+  // 8r..8r+7 read row r's 16-B chunks), so each warp instruction moves 512 B.  A B200 SM keeps
+  // only a few zero-copy instructions in flight: 16-B requests gather ~4x faster per SM than
+  // 4-B ones (csrc/probe measurement in DESIGN.md §6c), which matters when a layer has few DEC CTAs
+  // (tensor-parallel shards).  Lane l accumulates the 32 columns (l & 7) * 32 .. +31 of its rows;
+  // store_part folds the 4 row groups with two shuffles (fixed order).
+  constexpr bool kWide = RBITS == 4;
+#else
+  constexpr bool kWide = false;
+#endif
+  constexpr int kAccN = kWide ? 32 : 8;
   auto issue = [&](int it, int bsel) {  // all zero-copy reads of item `it` (async, into smem)
     const int i = it % ns, j = it / ns;
+    if constexpr (kWide) {
+      const int segc0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols;
+      const bool cv = segc0 + (lane & 7) * 32 < p.d_out;
+      const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, k_local);
+      uint4* dst = reinterpret_cast<uint4*>(stage) + bsel * p.rpi * 8 + lane;
+#pragma unroll
+      for (int r4 = 0; r4 < kGR / 4; ++r4) {
+        const int rr = r4 * 4 + (lane >> 3), e = e0 + rr;
+        if (rr < p.rpi && e < e1 && cv) {
+          const uint8_t* rowp = p.r_rows + (size_t)sidx[share_r + e * share_n] * p.r_row_bytes;
+          cp_async_16_ca(dst + r4 * 32, rowp + (segc0 >> 1) + (lane & 7) * 16);
+        }
+      }
+      cp_async_commit();
+      return;
+    }
     const int col0 = ((int)blockIdx.x + i * p.n_dec) * kSegCols + lane * 8;
     const bool cv = col0 < p.d_out;
     const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, k_local);
@@ -201,9 +230,32 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     }
     cp_async_commit();
   };
-  auto consume = [&](int it, int bsel, float* acc) {  // decode + FHFMA into acc[8]
+  auto consume = [&](int it, int bsel, float* acc) {  // decode + FHFMA into acc[kAccN]
     const int j = it / ns;
     const int e0 = j * p.rpi, e1 = min(e0 + p.rpi, k_local);
+    if constexpr (kWide) {
+      const uint4* src4 = reinterpret_cast<const uint4*>(stage) + bsel * p.rpi * 8 + lane;
+#pragma unroll
+      for (int r4 = 0; r4 < kGR / 4; ++r4) {
+        const int rr = r4 * 4 + (lane >> 3), e = e0 + rr;
+        if (rr < p.rpi && e < e1) {
+          const uint16_t xv = sxs[share_r + e * share_n];
+          const uint4 w4 = src4[r4 * 32];
+          const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t cq[4];
+            decode_rq_word(wd[q], cq);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              acc[8 * q + 2 * u] = fhfma_s_lo(xv, cq[u], acc[8 * q + 2 * u]);
+              acc[8 * q + 2 * u + 1] = fhfma_s_hi(xv, cq[u], acc[8 * q + 2 * u + 1]);
+            }
+          }
+        }
+      }
+      return;
+    }
     const Vec* src = stage + bsel * p.rpi * 32 + lane;
 #pragma unroll
     for (int r = 0; r < kGR; ++r) {
@@ -229,6 +281,21 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
   // accumulates them in registers and leaves ONE partial (slot = warp); otherwise one partial
   // per item (slot = row chunk j).  p.nparts = partials per segment (combined in slot order).
   auto store_part = [&](int i, int slot, float* acc) {
+    if constexpr (kWide) {  // fold the 4 row groups: (g0 + g1) + (g2 + g3), then lanes 0..7 store
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 8);
+        acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 16);
+      }
+      if (lane < 8) {
+        float* pp = spart + ((size_t)i * p.nparts + slot) * kSegCols + lane * 32;
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) *reinterpret_cast<float4*>(pp + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+      return;
+    }
     float* pp = spart + ((size_t)i * p.nparts + slot) * kSegCols + lane * 8;
     *reinterpret_cast<float4*>(pp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     *reinterpret_cast<float4*>(pp + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
@@ -254,6 +321,9 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
         Vec* dummy;
         int ns, lane;
         __device__ __forceinline__ bool on() const { return pp->early_reads != 0; }
+        __device__ __forceinline__ int cap() const { return pp->early_cap & 0xffff; }
+        // the finisher warp issues none (its R placement does not queue behind zero-copy requests)
+        __device__ __forceinline__ bool spare_finisher() const { return (pp->early_cap >> 16) != 0; }
         __device__ __forceinline__ void operator()(int row) const {
           const uint8_t* rowp = pp->r_rows + (size_t)row * pp->r_row_bytes;
           for (int i = 0; i < ns; ++i) {
@@ -319,7 +389,9 @@ __device__ __forceinline__ void dec_cta(const LinearParams& p, uint8_t* smem, in
     if (tr && warp == 0 && lane == 0) tr[2] = clock64();  // DEC CTAs: cycle stamps in slots 2-4, 10
     issue(it, 0);
   }
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float acc[kAccN];
+#pragma unroll
+  for (int c = 0; c < kAccN; ++c) acc[c] = 0.f;
   const bool one_seg = p.one_seg;  // plan-wide: every DEC CTA has <= 1 segment
   const bool had_item = it < n_items;
   for (int b = 0; it < n_items; b ^= 1, it += nw) {

@@ -448,6 +448,8 @@ __device__ __forceinline__ void select_wait_rest(const SelectSmemS* S) {
 
 struct NoEarly {
   __device__ __forceinline__ bool on() const { return false; }
+  __device__ __forceinline__ int cap() const { return 0; }
+  __device__ __forceinline__ bool spare_finisher() const { return false; }
   __device__ __forceinline__ void operator()(int) const {}
 };
 template <int MAXC, typename Early = NoEarly>
@@ -550,18 +552,24 @@ __device__ __forceinline__ int select_split(const uint16_t* __restrict__ x, int 
 #ifndef DECDEC_NO_EARLY
   // every D key of the warp handed to `early` warp-collectively before barrier 2 (the caller
   // starts fetching those rows while the rest of the selection runs)
-  if (early.on())
-  for (int m = 0; m < MAXC; ++m) {
-    uint32_t any = __ballot_sync(0xffffffffu, dmask[m] != 0u);
-    while (any) {
-      const int src = __ffs(any) - 1;
-      any &= any - 1;
-      uint32_t bits = __shfl_sync(0xffffffffu, dmask[m], src);
-      const int base = 8 * (__shfl_sync(0xffffffffu, c0, src) + m);
-      while (bits) {
-        const int jj = __ffs(bits) - 1;
-        bits &= bits - 1;
-        early(base + jj);
+  // At most early.cap() rows per warp (0 = all): a warp's zero-copy requests in flight are few,
+  // and a warp that waits to issue more stalls the selection at barrier 2.
+  if (early.on() && (wid != finisher || !early.spare_finisher())) {
+    const int cap = early.cap();
+    int issued = 0;
+    for (int m = 0; m < MAXC; ++m) {
+      uint32_t any = __ballot_sync(0xffffffffu, dmask[m] != 0u);
+      while (any && (cap == 0 || issued < cap)) {
+        const int src = __ffs(any) - 1;
+        any &= any - 1;
+        uint32_t bits = __shfl_sync(0xffffffffu, dmask[m], src);
+        const int base = 8 * (__shfl_sync(0xffffffffu, c0, src) + m);
+        while (bits && (cap == 0 || issued < cap)) {
+          const int jj = __ffs(bits) - 1;
+          bits &= bits - 1;
+          early(base + jj);
+          ++issued;
+        }
       }
     }
   }

@@ -21,10 +21,12 @@ ap.add_argument("--model", default="llama3_8b")
 ap.add_argument("--bits", type=int, default=3)
 ap.add_argument("--kchunk", type=int, default=0)
 ap.add_argument("--blocks", type=int, default=4)
+ap.add_argument("--shard-of", type=int, default=1, help="rank 0's 1/P output-feature shard of every layer")
 a = ap.parse_args()
 layers, hosts, xs, ys, meta = [], [], [], [], []
 for b in range(a.blocks):
     for name, d_in, d_out in model_layers(a.model, fused=True):
+        d_out //= a.shard_of
         g = gen_perf_layer_device(d_in, d_out, a.bits, layer_seed("ts", b, name))
         rb = d_out // 2
         off = (d_in * rb + 255) // 256 * 256
