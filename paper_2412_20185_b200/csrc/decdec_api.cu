@@ -45,6 +45,7 @@ struct Plan {
   int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, n_dec;  // grid = GEMV CTAs (+ n_dec DEC CTAs)
   int n_seg, rpi, gws, nparts, one_seg;  // DEC: output segments, rows per gather item, items and partials per segment
   int early_reads, early_cap;            // DEC: read the D rows during the selection (linear.cuh)
+  double r_ratio;                        // PCIe / HBM roofline time of the call
   uint32_t stage_bytes, off_s, off_z, off_sel, off_x, off_part, off_rsc, off_stage;
   size_t smem;
 };
@@ -232,6 +233,7 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
       if (k_sel > 0 && !plan_dec(d_out, k_sel, sel_len, 1 + nc, r_bits == 16 ? kGatherRows16 : kGatherRows4, r_ratio, &p))
         continue;
       p.early_reads = k_sel > 0 && early_reads(r_ratio);
+      p.r_ratio = k_sel > 0 ? r_ratio : 0.0;
       p.early_cap = early_cap();
       const int max_grid = sms - p.n_dec;
       if (max_grid <= 0) continue;
@@ -551,6 +553,18 @@ decdec_status launch_gemv(const GemvPlan& pl, int bits, bool pdl, cudaStream_t s
   else if (pair) e = bits == 3 ? cudaLaunchKernelEx(&cfg, k_gemv16<3, 1>, pl.gp) : cudaLaunchKernelEx(&cfg, k_gemv16<4, 1>, pl.gp);
   else e = bits == 3 ? cudaLaunchKernelEx(&cfg, k_gemv16<3, 0>, pl.gp) : cudaLaunchKernelEx(&cfg, k_gemv16<4, 0>, pl.gp);
   return cuda_status(e);
+}
+
+// DECDEC_STACK_FIT: 0 = off, else the least % of a compensated layer's planned GEMV CTAs kept when
+// its grid is shrunk to fit beside the previous layer's DEC CTAs (stack_create)
+int stack_fit() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DECDEC_STACK_FIT");
+    env = e ? atoi(e) : 50;
+    if (env < 0) env = 0;
+  }
+  return env;
 }
 
 // DECDEC_L2PF_NEXT=1 enables the stack executor's cross-layer L2 prefetch (A/B only)
@@ -892,6 +906,24 @@ decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const i
   if (s != DECDEC_OK) {
     delete[] P;
     return s;
+  }
+  // A compensated layer's launch is cooperative: the whole grid must be resident at once, so a
+  // 148-CTA grid waits until the previous layer's DEC CTAs (still combining) have left.  Shrinking
+  // its GEMV CTAs to fit beside them lets it launch -- and run its prologue -- while the previous
+  // layer finishes.  Only where the GEMV has slack (PCIe/HBM roofline ratio r >= 2: the PCIe
+  // gather bounds the call), and not below stack_fit() % of the planned GEMV CTAs.  Measured
+  // (1x B200, Llama-3-8B step, alternating runs): k_chunk 21 -3 %, 32 -2 %; applied at k_chunk 8
+  // (r ~1.3) it cost +2 %, hence the r bound.  DECDEC_STACK_FIT=0 turns it off (A/B).
+  if (stack_fit() > 0 && n_layers > 1) {
+    const int sms = device_sms();
+    for (int i = 0; i < n_layers; ++i) {
+      Prepared& Q = P[i];
+      if (Q.gemv || Q.p.k_sel == 0 || Q.pl.r_ratio < 2.0) continue;
+      const Prepared& Pv = P[(i + n_layers - 1) % n_layers];  // the graph replays cyclically
+      const int prev_dec = (Pv.gemv || Pv.p.k_sel == 0) ? 0 : Pv.pl.n_dec;
+      const int cap = sms - prev_dec - Q.pl.n_dec;
+      if (Q.pl.grid > cap && cap * 100 >= stack_fit() * Q.pl.grid) Q.pl.grid = cap;
+    }
   }
   if (l2_next_prefetch() && n_layers > 1) {
     for (int i = 0; i < n_layers; ++i) {
