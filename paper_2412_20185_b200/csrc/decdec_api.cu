@@ -45,7 +45,7 @@ struct Plan {
   int G, NKW, NSLOTS, RPS, TR, NC, stages, n_tiles, grid, n_dec;  // grid = GEMV CTAs (+ n_dec DEC CTAs)
   int n_seg, rpi, gws, nparts, one_seg;  // DEC: output segments, rows per gather item, items and partials per segment
   int early_reads, early_cap;            // DEC: read the D rows during the selection (linear.cuh)
-  double r_ratio;                        // PCIe / HBM roofline time of the call
+  double r_ratio, t_hbm_us;              // PCIe / HBM roofline time of the call; HBM roofline (us)
   uint32_t stage_bytes, off_s, off_z, off_sel, off_x, off_part, off_rsc, off_stage;
   size_t smem;
 };
@@ -73,7 +73,15 @@ int dec_ctas(int warps_per_cta, double r) {
     env = e ? atoi(e) : 0;
   }
   if (env > 0) return env;
-  const int base = r < 1.0 ? 272 : (r < 2.5 ? 544 : 1088);  // gather warps
+  // r >= 2.5: 48 CTAs of 17 warps since the 16-B gather and the fitted stack grids (k_chunk 21
+  // -1.7 % vs 64, profiles/r02_s3_experiments.json); DECDEC_DEC_WARPS_HI overrides
+  static int hi = -1;
+  if (hi < 0) {
+    const char* e = getenv("DECDEC_DEC_WARPS_HI");
+    hi = e ? atoi(e) : 816;
+    if (hi < 17) hi = 17;
+  }
+  const int base = r < 1.0 ? 272 : (r < 2.5 ? 544 : hi);  // gather warps
   int n = (base + warps_per_cta - 1) / warps_per_cta;
   return n < 2 ? 2 : (n > 64 ? 64 : n);
 }
@@ -234,6 +242,7 @@ decdec_status make_plan(int d_in, int d_out, int bits, int k_sel, Plan* pl, int 
         continue;
       p.early_reads = k_sel > 0 && early_reads(r_ratio);
       p.r_ratio = k_sel > 0 ? r_ratio : 0.0;
+      p.t_hbm_us = t_hbm / 1000.0;
       p.early_cap = early_cap();
       const int max_grid = sms - p.n_dec;
       if (max_grid <= 0) continue;
@@ -922,7 +931,16 @@ decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const i
       const Prepared& Pv = P[(i + n_layers - 1) % n_layers];  // the graph replays cyclically
       const int prev_dec = (Pv.gemv || Pv.p.k_sel == 0) ? 0 : Pv.pl.n_dec;
       const int cap = sms - prev_dec - Q.pl.n_dec;
-      if (Q.pl.grid > cap && cap * 100 >= stack_fit() * Q.pl.grid) Q.pl.grid = cap;
+      if (Q.pl.grid <= cap || cap * 100 < stack_fit() * Q.pl.grid) continue;
+      // and only if the shrunk GEMV still hides under the compensation: GEMV time modelled from
+      // the HBM roofline at ~60 % efficiency x the lanes a row team uses (3-bit decode is issue
+      // bound; G = 40 teams idle 24 of 64 lanes), compensation time from the PCIe roofline at
+      // ~75 % + ~4 us fixed (§6c); keep 20 % margin.  Phi-3's gate/up layer (G = 40) fails it:
+      // fitted, it turned the Phi-3 k_chunk-21 step 11 % slower.
+      const double lane_eff = Q.pl.NKW ? (double)Q.pl.G / (32.0 * Q.pl.NKW) : 1.0;
+      const double t_gemv = Q.pl.t_hbm_us / (0.6 * lane_eff * cap / sms);
+      const double t_dec = Q.pl.t_hbm_us * Q.pl.r_ratio / 0.75 + 4.0;
+      if (t_gemv <= 0.8 * t_dec) Q.pl.grid = cap;
     }
   }
   if (l2_next_prefetch() && n_layers > 1) {
