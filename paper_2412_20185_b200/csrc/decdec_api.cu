@@ -576,6 +576,17 @@ int stack_fit() {
   return env;
 }
 
+// DECDEC_STACK_FIT_RMIN (x100): the least PCIe/HBM roofline ratio of a call the fit applies to
+double stack_fit_rmin() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DECDEC_STACK_FIT_RMIN");
+    env = e ? atoi(e) : 0;  // measured: 0 (the time model alone) vs 2.0: k_chunk 1 -2.6 %, 4 -2.2 %,
+    if (env < 0) env = 0;   // 8 -1.6 %, 12/21 +-0.6 % (the small layers' GEMV hides under the
+  }                         // compensation latency at any k)
+  return env / 100.0;
+}
+
 // DECDEC_L2PF_NEXT=1 enables the stack executor's cross-layer L2 prefetch (A/B only)
 bool l2_next_prefetch() {
   static int env = -1;
@@ -919,15 +930,15 @@ decdec_status stack_create(const decdec_layer* layers, int32_t n_layers, const i
   // A compensated layer's launch is cooperative: the whole grid must be resident at once, so a
   // 148-CTA grid waits until the previous layer's DEC CTAs (still combining) have left.  Shrinking
   // its GEMV CTAs to fit beside them lets it launch -- and run its prologue -- while the previous
-  // layer finishes.  Only where the GEMV has slack (PCIe/HBM roofline ratio r >= 2: the PCIe
-  // gather bounds the call), and not below stack_fit() % of the planned GEMV CTAs.  Measured
-  // (1x B200, Llama-3-8B step, alternating runs): k_chunk 21 -3 %, 32 -2 %; applied at k_chunk 8
-  // (r ~1.3) it cost +2 %, hence the r bound.  DECDEC_STACK_FIT=0 turns it off (A/B).
+  // layer finishes.  Only where the GEMV has slack (time model below), and not below stack_fit()
+  // % of the planned GEMV CTAs.  Measured (1x B200, alternating runs): Llama-3-8B k_chunk 21
+  // -7 %, 12 -6 %, 4 -2 % vs no fit (profiles/r02_s3_experiments.json).  DECDEC_STACK_FIT=0
+  // turns it off (A/B).
   if (stack_fit() > 0 && n_layers > 1) {
     const int sms = device_sms();
     for (int i = 0; i < n_layers; ++i) {
       Prepared& Q = P[i];
-      if (Q.gemv || Q.p.k_sel == 0 || Q.pl.r_ratio < 2.0) continue;
+      if (Q.gemv || Q.p.k_sel == 0 || Q.pl.r_ratio < stack_fit_rmin()) continue;
       const Prepared& Pv = P[(i + n_layers - 1) % n_layers];  // the graph replays cyclically
       const int prev_dec = (Pv.gemv || Pv.p.k_sel == 0) ? 0 : Pv.pl.n_dec;
       const int cap = sms - prev_dec - Q.pl.n_dec;
