@@ -86,10 +86,10 @@ int dec_ctas(int warps_per_cta, double r) {
   return n < 2 ? 2 : (n > 64 ? 64 : n);
 }
 
-// Early D-row reads (linear.cuh dec_cta): on for calls whose PCIe/HBM roofline ratio r lies in
-// [kEarlyLo, kEarlyHi] -- measured on the Llama-3-8B step (1x B200, same box A/B): k_chunk 21
-// (r ~3.4) -3.6 %, k_chunk 8 (r ~1.3) +-0, k_chunk 1-4 (r < 0.7) +2-3 %, k_chunk 32 (r ~5.2)
-// +0.6 %.  DECDEC_EARLY=0|1 forces it.
+// Early D-row reads (linear.cuh dec_cta): on for calls whose PCIe/HBM roofline ratio r lies in a
+// window (early_reads() below) -- first measured with the 4-B gather (k_chunk 21 -3.6 %, k_chunk
+// 1-4 +2-3 %), re-measured with the 16-B gather and the fitted step graph.  DECDEC_EARLY=0|1
+// forces it.
 // Early reads per warp at most (DECDEC_EARLY_CAP, 0 = every D row the warp holds): an SM keeps
 // few zero-copy requests in flight, so a warp with many D rows stalls in its early-read loop and
 // holds up the selection's barrier 2 (d layer: D placed at ~19000 instead of ~12000 cycles).
@@ -114,7 +114,11 @@ int early_reads(double r) {
     env = e ? atoi(e) : -1;
   }
   if (env >= 0) return env > 0;
-  return r >= 1.5 && r <= 4.5;
+  // window re-measured with the 16-B gather and the fitted step graph (forced on vs this window,
+  // profiles/r02_s3_experiments.json): k_chunk 8 (r ~1.3) -2.0 %, 32 (r ~5.2) -3.8 %, 48 -1.2 %,
+  // 64 +-0.5 %, 82 (r ~13) +2.8 %, 4 (r ~0.6) +-0.1 %; with [1.0, 9.0] vs [1.5, 4.5]: 8 -1.8 %,
+  // 32 -3.8 %, 48 -1.2 %, Phi-3 32 -3.4 %, 6 (r ~1.0) +0.5 % -> lower bound 1.1
+  return r >= 1.1 && r <= 9.0;
 }
 
 // DEC CTA layout: CTA c owns segments c, c + n_dec, ...; a segment's k_sel rows are split in
