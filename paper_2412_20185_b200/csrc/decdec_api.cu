@@ -81,7 +81,13 @@ int dec_ctas(int warps_per_cta, double r) {
     hi = e ? atoi(e) : 816;
     if (hi < 17) hi = 17;
   }
-  const int base = r < 1.0 ? 272 : (r < 2.5 ? 544 : hi);  // gather warps
+  static int mid = -1;  // DECDEC_DEC_WARPS_MID: gather warps for 1 <= r < 2.5
+  if (mid < 0) {
+    const char* e = getenv("DECDEC_DEC_WARPS_MID");
+    mid = e ? atoi(e) : 544;
+    if (mid < 17) mid = 17;
+  }
+  const int base = r < 1.0 ? 272 : (r < 2.5 ? mid : hi);  // gather warps
   int n = (base + warps_per_cta - 1) / warps_per_cta;
   return n < 2 ? 2 : (n > 64 ? 64 : n);
 }
