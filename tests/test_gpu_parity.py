@@ -444,6 +444,29 @@ def test_stack_graph_matches_per_layer_calls():
     st.close()
 
 
+def test_stack_fitted_grids_match_per_layer_calls():
+    """Llama-sized qkv/o layers at k_chunk 21: in the stack graph the o layer's cooperative grid is
+    shrunk to fit beside qkv's DEC CTAs (decdec_api.cu stack_create, the time model admits it);
+    the rows' arithmetic does not depend on the grid, so y is bit-identical to per-layer calls."""
+    shapes = [(4096, 6144), (4096, 4096), (4096, 6144), (4096, 4096)]
+    lins, xs = [], []
+    for i, (d_in, d_out) in enumerate(shapes):
+        L = gen_perf_layer(d_in, d_out, 3, seed=300 + i)
+        lins.append(dd.QuantLinear.from_codes(L["q"], L["s"], L["z"], 3, rc=L["rc"], rS=L["rS"]))
+        xs.append(to_dev(gen_activations(d_in, 1, seed=400 + i)[0]))
+    ks = [oracle.k_from_kchunk(21, d_in) for d_in, _ in shapes]
+    ws = dd.Workspace(max(ks), 6144)
+    ref = [lin(x, k, workspace=ws).clone() for lin, x, k in zip(lins, xs, ks)]
+    ys = [torch.empty(d_out, dtype=torch.float16, device=DEV) for _, d_out in shapes]
+    st = dd.Stack(lins, ks, xs, ys, ws)
+    for _ in range(3):
+        st.launch()
+    torch.cuda.synchronize()
+    for a, b in zip(ys, ref):
+        assert torch.equal(a, b)
+    st.close()
+
+
 # ------------------------------------------------------------------ TP entry points (1 rank)
 def _comm1():
     assert dd.decdec_nccl_version() > 0, "NCCL could not be loaded by libdecdec"
